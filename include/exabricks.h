@@ -1,0 +1,151 @@
+/*
+ * exabricks.h — C ABI of libexabricks.so, the B200-native (sm_100a) ExaBricks
+ * hot path.  Plain pointers and sizes only; no torch / C++ types.
+ *
+ * The reference (`amrvol`, R/ = /root/reference/pkg/src/amrvol/) is Python +
+ * numba with no FFI of its own; its operator boundary is the Python API plus
+ * the numba kernel argument lists.  Each entry point below replaces one of
+ * those (cited per function).  The Python package `paper_2009_03076_b200`
+ * binds this header with ctypes and keeps the reference's Python signatures;
+ * INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - return 0 on success, a negative XB_ERR_* code on failure; the message is
+ *     available from xb_last_error() (thread-local);
+ *   - host arrays are borrowed for the duration of the call;
+ *   - objects (xb_model, xb_regions, xb_active) own device memory on the CUDA
+ *     device they were created on and are immutable after creation, so any
+ *     number of threads may render from them concurrently (the reference's
+ *     service renders outside its lock, R/service.py:166-176);
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ */
+#ifndef EXABRICKS_H
+#define EXABRICKS_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library builds with -fvisibility=hidden */
+#endif
+
+#define XB_OK 0
+#define XB_ERR_CUDA (-1)
+#define XB_ERR_ARG (-2)
+#define XB_ERR_INVALID_CELLS (-3) /* build_bricks input fails validate_cells */
+#define XB_ERR_RANGE (-4)
+#define XB_ERR_NO_TREE (-5)
+#define XB_ERR_INTERNAL (-6)
+
+typedef struct xb_model xb_model;     /* AmrModel on the device (R/model.py:250-343) */
+typedef struct xb_regions xb_regions; /* RegionSet + its k-d tree (R/regions.py:35-79) */
+typedef struct xb_active xb_active;   /* pruned region set = RegionBvh (R/accel.py:125-155) */
+
+const char* xb_last_error(void);
+int xb_abi_version(void);
+int xb_device_count(int32_t* n);
+
+/* ---- bricks: build_bricks(cells, BrickBuildParams) R/bricks.py:104-228 ---- */
+/* values: (n, n_fields) row-major float32, as CellList.values (R/model.py:135-138).
+ * XB_ERR_INVALID_CELLS when validate_cells (R/model.py:392-457) would fail. */
+int xb_build_bricks(const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* level, const float* values,
+                    int64_t n, int32_t n_fields, int32_t max_brick_width, int32_t keep_split_tree, int32_t device,
+                    xb_model** out);
+/* AmrModel(field_names, brick_lower, brick_level, brick_dims, scalars) R/model.py:257-267; scalars (F, N). */
+int xb_model_upload(const int32_t* lower, const int32_t* level, const int32_t* dims, const float* scalars,
+                    int64_t n_bricks, int64_t n_cells, int32_t n_fields, int32_t device, xb_model** out);
+int xb_model_info(const xb_model* m, int64_t* n_bricks, int64_t* n_cells, int32_t* n_fields, int64_t* n_tree_nodes);
+int xb_model_download(const xb_model* m, int32_t* lower, int32_t* level, int32_t* dims, int64_t* offset,
+                      float* scalars);
+/* SplitTree arrays (R/bricks.py:45-68), preorder; only when built with keep_split_tree */
+int xb_model_download_tree(const xb_model* m, int32_t* axis, double* pos, int32_t* left, int32_t* right,
+                           int32_t* brick_start, int32_t* brick_count, double* box_lo, double* box_hi,
+                           double* max_half);
+void xb_model_free(xb_model* m);
+
+/* ---- regions: build_regions(model) R/regions.py:90-213 ---- */
+int xb_build_regions(const xb_model* m, xb_regions** out);
+int xb_regions_info(const xb_regions* r, int64_t* n_regions, int64_t* n_ids, int64_t* n_kd_nodes, int32_t* kd_depth);
+/* value_range (R, F, 2) float64, finest_width (R) float64 — RegionSet layout */
+int xb_regions_download(const xb_regions* r, double* lo, double* hi, int64_t* brick_off, int32_t* brick_ids,
+                        double* value_range, double* finest_width);
+void xb_regions_free(xb_regions* r);
+
+/* ---- active sets: build_volume_bvh / build_iso_bvh / build_all_regions_bvh R/accel.py:227-247 ---- */
+/* rgba: 256x4 float64 ramp (TransferFunction.rgba, R/accel.py:38-88) */
+int xb_active_volume(const xb_regions* r, int32_t field, double tf_lo, double tf_hi, const double* rgba,
+                     xb_active** out);
+int xb_active_iso(const xb_regions* r, int32_t field, double iso_value, xb_active** out);
+int xb_active_all(const xb_regions* r, xb_active** out);
+int xb_active_info(const xb_active* a, int64_t* n_active, double* build_ms);
+int xb_active_prims(const xb_active* a, int32_t* prims); /* ascending active region ids */
+void xb_active_free(xb_active* a);
+
+/* ---- render_frame R/render.py:654-691 (kernel body R/render.py:521-578) ---- */
+typedef struct {
+    int32_t width, height;
+    double position[3];
+    double right[3], up[3], forward[3]; /* Camera.basis(), R/render.py:73-79 */
+    double tan_half;                    /* tan(radians(fov_y) / 2) */
+    double aspect;                      /* width / height */
+} xb_camera;
+
+typedef struct {
+    double samples_per_cell, rate_scale, early_term_threshold; /* MarchParams, R/render.py:92-116 */
+    uint64_t seed;
+    int32_t gradient_mode; /* GRADIENT_MODES: 0 none, 1 analytic, 2 central, 3 clampedCentral */
+    int32_t n_planes;      /* clip planes (n, c): keep dot(n, x) <= c */
+    double planes[6][4];
+    int32_t iso_on;
+    double iso_value;
+    double iso_rgb[3]; /* ISO_COLOR, R/render.py:47 */
+    double tf_lo, tf_hi;
+    double tf_rgba[1024];
+} xb_march;
+
+/* Render the tiles of `tile_rank` out of `tile_world` (16x8-pixel tiles dealt
+ * round-robin; world = 1 renders the frame).  rgba8: host or device; with
+ * world == 1 it is the (H, W, 4) image, otherwise the rank's packed tiles
+ * (xb_tile_count() tiles x 128 px x 4 B).  rgba_f64 / px_counts (int32
+ * regions, samples per pixel): optional parity outputs, same layout, host or
+ * device.  stats (host, may be NULL): [regions, samples, algorithmic bytes]
+ * (bytes only when count_bytes != 0).  `vol` may not be NULL; `iso` may. */
+int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* vol, const xb_active* iso,
+              const xb_camera* cam, const xb_march* mp, int32_t tile_rank, int32_t tile_world, void* rgba8,
+              double* rgba_f64, int32_t* px_counts, int64_t* stats, int32_t count_bytes, void* stream);
+int xb_tile_count(int32_t width, int32_t height, int32_t rank, int32_t world, int64_t* n_tiles, int32_t* tile_px);
+/* gathered packed tiles (rank-major, tiles_per_rank each) -> (H, W, 4) image; device pointers */
+int xb_unpack_tiles(const void* packed, int64_t tiles_per_rank, int32_t world, int32_t width, int32_t height,
+                    void* rgba8, void* stream);
+
+/* ---- single rays: integrate_ray R/render.py:613-632, iso_intersect 635-651 ---- */
+/* host arrays; o, d (n,3) (d normalised by the caller), t0/t1/rho (n).
+ * out (n,4) RGBA float64, counts (n,2) int64 regions/samples. */
+int xb_integrate_rays(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* vol,
+                      const xb_march* mp, int64_t n, const double* o, const double* d, const double* t0,
+                      const double* t1, const double* rho, double* out, int64_t* counts);
+/* out (n,4): t_hit, gx, gy, gz ; hit (n) */
+int xb_iso_rays(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* iso, const xb_march* mp,
+                int64_t n, const double* o, const double* d, const double* t0, const double* t1, const double* rho,
+                double* out, int32_t* hit);
+
+/* ---- point reconstruction: basis_sample_region / gradient_analytic R/sampling.py:281-353 ---- */
+/* region: per-point region id, or NULL to locate each point (point_to_region, R/regions.py:216-220).
+ * acc (n, 9): num, den, [shifted num, dn(3), dd(3) when want_grad] (_gradient_bricks accumulators) */
+int xb_sample_points(const xb_model* m, const xb_regions* r, int32_t field, int64_t n, const double* p,
+                     const int32_t* region, int32_t want_grad, int32_t* region_out, double* acc);
+/* basis_sample_oracle over the canonical cell order (R/sampling.py:291-298): out (n,2) num, den */
+int xb_sample_scan(const xb_model* m, int32_t field, int64_t n, const double* p, double* out);
+/* iterate_intervals R/accel.py:414-424 for n rays: up to cap intervals each (t_in, t_out, region), count */
+int xb_trace_intervals(const xb_model* m, const xb_regions* r, const xb_active* a, int64_t n, const double* o,
+                       const double* d, double t_start, double t_max, int32_t cap, double* t_in, double* t_out,
+                       int32_t* region, int32_t* count);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXABRICKS_H */

@@ -1,0 +1,572 @@
+// abi.cu — extern "C" entry points of libexabricks (include/exabricks.h).
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include "../../include/exabricks.h"
+#include "accel.cuh"
+#include "render.cuh"
+
+namespace xb {
+bool build_bricks_device(const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* l, const float* v,
+                         int64_t n, int F, int64_t maxw, bool keep_tree, int device, DevModel& m, cudaStream_t s);
+void finish_model(DevModel& m, cudaStream_t s);
+void build_regions_device(const DevModel& m, DevRegions& out, cudaStream_t s);
+}  // namespace xb
+
+struct xb_model {
+    xb::DevModel m;
+};
+struct xb_regions {
+    xb::DevRegions r;
+    int64_t model_bricks = 0;
+};
+struct xb_active {
+    xb::DevActive a;
+    const xb_regions* owner = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return XB_OK;
+    } catch (const xb::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return XB_ERR_INTERNAL;
+    } catch (...) {
+        g_err = "unknown error";
+        return XB_ERR_INTERNAL;
+    }
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// per-call owned stream for synchronous builders
+struct OwnedStream {
+    cudaStream_t s = nullptr;
+    OwnedStream() { XB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+    ~OwnedStream() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
+    XB_CHECK(m && r, XB_ERR_ARG, "null model or regions");
+    XB_CHECK(r->model_bricks == m->m.n_bricks, XB_ERR_ARG, "regions were built for a different model");
+    XB_CHECK(field >= 0 && field < std::max(m->m.n_fields, 1), XB_ERR_ARG, "field index out of range");
+    XB_CHECK(r->r.has_tree, XB_ERR_NO_TREE, "regions carry no k-d tree");
+    XB_CHECK(r->r.kd_depth <= xb::kKdStack, XB_ERR_RANGE, "region k-d tree deeper than the traversal stack");
+    xb::SceneView S;
+    S.brick_a = m->m.brick_a.p;
+    S.brick_m = m->m.brick_m.p;
+    S.vals = m->m.vals.p + (size_t)field * (size_t)m->m.n_cells;
+    S.rec = r->r.rec.p;
+    S.rids = r->r.ids.p;
+    S.kd = r->r.kd.p;
+    for (int a = 0; a < 3; a++) {
+        S.root_lo[a] = r->r.root_lo[a];
+        S.root_hi[a] = r->r.root_hi[a];
+    }
+    S.n_kd = r->r.n_regions > 0 ? r->r.n_kd : 0;
+    return S;
+}
+
+void fill_march(xb::MarchConst& M, const xb_march* mp) {
+    M.spc = mp->samples_per_cell;
+    M.rate = mp->rate_scale;
+    M.early = mp->early_term_threshold;
+    M.seed = mp->seed;
+    M.grad_mode = mp->gradient_mode;
+    XB_CHECK(mp->gradient_mode >= 0 && mp->gradient_mode <= 3, XB_ERR_ARG, "unknown gradient mode");
+    XB_CHECK(mp->n_planes >= 0 && mp->n_planes <= 6, XB_ERR_ARG, "at most 6 clip planes are supported");
+    M.n_planes = mp->n_planes;
+    for (int i = 0; i < 6; i++)
+        for (int c = 0; c < 4; c++) M.planes[i][c] = mp->planes[i][c];
+    M.iso_on = mp->iso_on;
+    M.iso_value = mp->iso_value;
+    for (int c = 0; c < 3; c++) M.iso_rgb[c] = mp->iso_rgb[c];
+    M.tf_lo = mp->tf_lo;
+    M.tf_hi = mp->tf_hi;
+}
+
+void check_active(const xb_active* a, const xb_regions* r, const char* what) {
+    XB_CHECK(a != nullptr, XB_ERR_ARG, std::string(what) + " active set is NULL");
+    XB_CHECK(a->owner == r, XB_ERR_ARG, std::string(what) + " active set belongs to other regions");
+}
+
+// device staging for an optional host/device output
+template <class T>
+struct OutBuf {
+    T* user = nullptr;
+    T* dev = nullptr;
+    size_t count = 0;
+    bool owned = false;
+    cudaStream_t s = nullptr;
+    void setup(T* p, size_t n, cudaStream_t st) {
+        user = p;
+        count = n;
+        s = st;
+        if (!p) return;
+        if (is_device_ptr(p)) {
+            dev = p;
+        } else {
+            XB_CUDA(cudaMallocAsync((void**)&dev, std::max<size_t>(n, 1) * sizeof(T), s));
+            owned = true;
+        }
+    }
+    void finish() {
+        if (owned && count) XB_CUDA(cudaMemcpyAsync(user, dev, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    ~OutBuf() {
+        if (owned && dev) cudaFreeAsync(dev, s);
+    }
+};
+
+int64_t tiles_for_rank(int W, int H, int rank, int world, int* tx_o, int* ty_o) {
+    const int tx = (W + xb::kTileW - 1) / xb::kTileW, ty = (H + xb::kTileH - 1) / xb::kTileH;
+    if (tx_o) *tx_o = tx;
+    if (ty_o) *ty_o = ty;
+    const int64_t total = (int64_t)tx * ty;
+    if (rank >= total) return 0;
+    return (total - rank + world - 1) / world;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* xb_last_error(void) { return g_err.c_str(); }
+
+int xb_abi_version(void) { return 1; }
+
+int xb_device_count(int32_t* n) {
+    return guarded([&] {
+        int c = 0;
+        XB_CUDA(cudaGetDeviceCount(&c));
+        *n = c;
+    });
+}
+
+int xb_build_bricks(const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* level, const float* values,
+                    int64_t n, int32_t n_fields, int32_t max_brick_width, int32_t keep_split_tree, int32_t device,
+                    xb_model** out) {
+    *out = nullptr;
+    return guarded([&] {
+        XB_CHECK(n >= 0 && n_fields >= 1, XB_ERR_ARG, "bad cell counts");
+        xb::DeviceGuard g(device);
+        OwnedStream st;
+        auto h = std::make_unique<xb_model>();
+        bool ok = xb::build_bricks_device(i, j, k, level, values, n, n_fields, max_brick_width, keep_split_tree != 0,
+                                          device, h->m, st.s);
+        XB_CHECK(ok, XB_ERR_INVALID_CELLS, "cells fail validation (alignment, duplicates or overlaps)");
+        *out = h.release();
+    });
+}
+
+int xb_model_upload(const int32_t* lower, const int32_t* level, const int32_t* dims, const float* scalars,
+                    int64_t n_bricks, int64_t n_cells, int32_t n_fields, int32_t device, xb_model** out) {
+    *out = nullptr;
+    return guarded([&] {
+        XB_CHECK(n_bricks >= 0 && n_cells >= 0 && n_fields >= 1, XB_ERR_ARG, "bad model sizes");
+        xb::DeviceGuard g(device);
+        OwnedStream st;
+        auto h = std::make_unique<xb_model>();
+        xb::DevModel& m = h->m;
+        m.device = device;
+        m.n_bricks = n_bricks;
+        m.n_fields = n_fields;
+        std::vector<int64_t> off(n_bricks + 1, 0);
+        for (int64_t b = 0; b < n_bricks; b++)
+            off[b + 1] = off[b] + (int64_t)dims[3 * b] * dims[3 * b + 1] * dims[3 * b + 2];
+        XB_CHECK(off[n_bricks] == n_cells, XB_ERR_ARG, "scalar array length does not match brick dims");
+        m.n_cells = n_cells;
+        m.lower.upload(lower, 3 * n_bricks, st.s);
+        m.level.upload(level, n_bricks, st.s);
+        m.dims.upload(dims, 3 * n_bricks, st.s);
+        m.offset.upload(off.data(), n_bricks + 1, st.s);
+        m.vals.alloc((size_t)n_fields * n_cells + 1);
+        if (n_cells) XB_CUDA(cudaMemcpyAsync(m.vals.p, scalars, (size_t)n_fields * n_cells * 4, cudaMemcpyHostToDevice, st.s));
+        xb::finish_model(m, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+        *out = h.release();
+    });
+}
+
+int xb_model_info(const xb_model* m, int64_t* n_bricks, int64_t* n_cells, int32_t* n_fields, int64_t* n_tree_nodes) {
+    return guarded([&] {
+        XB_CHECK(m, XB_ERR_ARG, "null model");
+        if (n_bricks) *n_bricks = m->m.n_bricks;
+        if (n_cells) *n_cells = m->m.n_cells;
+        if (n_fields) *n_fields = m->m.n_fields;
+        if (n_tree_nodes) *n_tree_nodes = m->m.n_tree;
+    });
+}
+
+int xb_model_download(const xb_model* m, int32_t* lower, int32_t* level, int32_t* dims, int64_t* offset,
+                      float* scalars) {
+    return guarded([&] {
+        XB_CHECK(m, XB_ERR_ARG, "null model");
+        xb::DeviceGuard g(m->m.device);
+        const auto& d = m->m;
+        const int64_t B = d.n_bricks;
+        if (lower) d.lower.download(lower, 3 * B);
+        if (level) d.level.download(level, B);
+        if (dims) d.dims.download(dims, 3 * B);
+        if (offset) d.offset.download(offset, B + 1);
+        if (scalars) d.vals.download(scalars, (size_t)d.n_fields * d.n_cells);
+        XB_CUDA(cudaStreamSynchronize(0));
+    });
+}
+
+int xb_model_download_tree(const xb_model* m, int32_t* axis, double* pos, int32_t* left, int32_t* right,
+                           int32_t* brick_start, int32_t* brick_count, double* box_lo, double* box_hi,
+                           double* max_half) {
+    return guarded([&] {
+        XB_CHECK(m, XB_ERR_ARG, "null model");
+        xb::DeviceGuard g(m->m.device);
+        const auto& d = m->m;
+        const int64_t T = d.n_tree;
+        d.t_axis.download(axis, T);
+        d.t_pos.download(pos, T);
+        d.t_left.download(left, T);
+        d.t_right.download(right, T);
+        d.t_bstart.download(brick_start, T);
+        d.t_bcount.download(brick_count, T);
+        d.t_lo.download(box_lo, 3 * T);
+        d.t_hi.download(box_hi, 3 * T);
+        d.t_mh.download(max_half, T);
+        XB_CUDA(cudaStreamSynchronize(0));
+    });
+}
+
+void xb_model_free(xb_model* m) {
+    if (!m) return;
+    int prev;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->m.device);
+    delete m;
+    cudaSetDevice(prev);
+}
+
+int xb_build_regions(const xb_model* m, xb_regions** out) {
+    *out = nullptr;
+    return guarded([&] {
+        XB_CHECK(m, XB_ERR_ARG, "null model");
+        xb::DeviceGuard g(m->m.device);
+        OwnedStream st;
+        auto h = std::make_unique<xb_regions>();
+        xb::build_regions_device(m->m, h->r, st.s);
+        h->model_bricks = m->m.n_bricks;
+        *out = h.release();
+    });
+}
+
+int xb_regions_info(const xb_regions* r, int64_t* n_regions, int64_t* n_ids, int64_t* n_kd_nodes, int32_t* kd_depth) {
+    return guarded([&] {
+        XB_CHECK(r, XB_ERR_ARG, "null regions");
+        if (n_regions) *n_regions = r->r.n_regions;
+        if (n_ids) *n_ids = r->r.n_ids;
+        if (n_kd_nodes) *n_kd_nodes = r->r.n_kd;
+        if (kd_depth) *kd_depth = r->r.kd_depth;
+    });
+}
+
+int xb_regions_download(const xb_regions* r, double* lo, double* hi, int64_t* brick_off, int32_t* brick_ids,
+                        double* value_range, double* finest_width) {
+    return guarded([&] {
+        XB_CHECK(r, XB_ERR_ARG, "null regions");
+        xb::DeviceGuard g(r->r.device);
+        const auto& d = r->r;
+        const int64_t R = d.n_regions;
+        if (lo) d.lo.download(lo, 3 * R);
+        if (hi) d.hi.download(hi, 3 * R);
+        if (brick_off) d.brick_off.download(brick_off, R + 1);
+        if (brick_ids) d.ids.download(brick_ids, d.n_ids);
+        if (value_range) d.vr64.download(value_range, 2 * R * d.n_fields);
+        if (finest_width) d.finest.download(finest_width, R);
+        XB_CUDA(cudaStreamSynchronize(0));
+    });
+}
+
+void xb_regions_free(xb_regions* r) {
+    if (!r) return;
+    int prev;
+    cudaGetDevice(&prev);
+    cudaSetDevice(r->r.device);
+    delete r;
+    cudaSetDevice(prev);
+}
+
+static int make_active(const xb_regions* r, int kind, int32_t field, double lo, double hi, const double* rgba,
+                       double iso, xb_active** out) {
+    *out = nullptr;
+    return guarded([&] {
+        XB_CHECK(r, XB_ERR_ARG, "null regions");
+        if (kind == 0) XB_CHECK(rgba && lo < hi, XB_ERR_ARG, "transfer function domain must satisfy lo < hi");
+        xb::DeviceGuard g(r->r.device);
+        OwnedStream st;
+        auto h = std::make_unique<xb_active>();
+        auto t0 = std::chrono::steady_clock::now();
+        xb::build_active(r->r, kind, field, lo, hi, rgba, iso, h->a, st.s);
+        h->a.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        h->owner = r;
+        *out = h.release();
+    });
+}
+
+int xb_active_volume(const xb_regions* r, int32_t field, double tf_lo, double tf_hi, const double* rgba,
+                     xb_active** out) {
+    return make_active(r, 0, field, tf_lo, tf_hi, rgba, 0.0, out);
+}
+
+int xb_active_iso(const xb_regions* r, int32_t field, double iso_value, xb_active** out) {
+    return make_active(r, 1, field, 0.0, 1.0, nullptr, iso_value, out);
+}
+
+int xb_active_all(const xb_regions* r, xb_active** out) { return make_active(r, 2, 0, 0.0, 1.0, nullptr, 0.0, out); }
+
+int xb_active_info(const xb_active* a, int64_t* n_active, double* build_ms) {
+    return guarded([&] {
+        XB_CHECK(a, XB_ERR_ARG, "null active set");
+        if (n_active) *n_active = a->a.n_active;
+        if (build_ms) *build_ms = a->a.build_ms;
+    });
+}
+
+int xb_active_prims(const xb_active* a, int32_t* prims) {
+    return guarded([&] {
+        XB_CHECK(a, XB_ERR_ARG, "null active set");
+        xb::DeviceGuard g(a->a.device);
+        a->a.prims.download(prims, a->a.n_active);
+        XB_CUDA(cudaStreamSynchronize(0));
+    });
+}
+
+void xb_active_free(xb_active* a) {
+    if (!a) return;
+    int prev;
+    cudaGetDevice(&prev);
+    cudaSetDevice(a->a.device);
+    delete a;
+    cudaSetDevice(prev);
+}
+
+int xb_tile_count(int32_t width, int32_t height, int32_t rank, int32_t world, int64_t* n_tiles, int32_t* tile_px) {
+    return guarded([&] {
+        XB_CHECK(width >= 1 && height >= 1 && world >= 1 && rank >= 0 && rank < world, XB_ERR_ARG, "bad tiling");
+        if (n_tiles) *n_tiles = tiles_for_rank(width, height, rank, world, nullptr, nullptr);
+        if (tile_px) *tile_px = xb::kTileW * xb::kTileH;
+    });
+}
+
+int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* vol, const xb_active* iso,
+              const xb_camera* cam, const xb_march* mp, int32_t tile_rank, int32_t tile_world, void* rgba8,
+              double* rgba_f64, int32_t* px_counts, int64_t* stats, int32_t count_bytes, void* stream) {
+    return guarded([&] {
+        XB_CHECK(cam && mp && rgba8, XB_ERR_ARG, "null camera, params or output");
+        XB_CHECK(cam->width >= 1 && cam->height >= 1, XB_ERR_ARG, "image must be at least 1x1 pixel");
+        XB_CHECK(tile_world >= 1 && tile_rank >= 0 && tile_rank < tile_world, XB_ERR_ARG, "bad tile rank/world");
+        xb::DeviceGuard g(m->m.device);
+        cudaStream_t s = (cudaStream_t)stream;
+        xb::RenderArgs* A = new xb::RenderArgs();  // 8.6 KB: keep off the stack
+        std::unique_ptr<xb::RenderArgs> hold(A);
+        A->S = scene_view(m, r, field);
+        check_active(vol, r, "volume");
+        A->vflags = vol->a.flags.p;
+        fill_march(A->M, mp);
+        A->M.iso_on = (mp->iso_on && iso) ? 1 : 0;
+        if (A->M.iso_on) check_active(iso, r, "iso");
+        A->iflags = A->M.iso_on ? iso->a.flags.p : vol->a.flags.p;
+        A->W = cam->width;
+        A->H = cam->height;
+        for (int a = 0; a < 3; a++) {
+            A->pos[a] = cam->position[a];
+            A->right[a] = cam->right[a];
+            A->up[a] = cam->up[a];
+            A->fwd[a] = cam->forward[a];
+        }
+        A->tan_half = cam->tan_half;
+        A->aspect = cam->aspect;
+        std::memcpy(A->tf, mp->tf_rgba, sizeof(A->tf));
+        int tx, ty;
+        const int64_t n_local = tiles_for_rank(cam->width, cam->height, tile_rank, tile_world, &tx, &ty);
+        A->tiles_x = tx;
+        A->tiles_y = ty;
+        A->tile_rank = tile_rank;
+        A->tile_world = tile_world;
+        A->packed = tile_world > 1;
+        const size_t npx = A->packed ? (size_t)n_local * xb::kTileW * xb::kTileH : (size_t)cam->width * cam->height;
+        OutBuf<uchar4> o8;
+        OutBuf<double4> of;
+        OutBuf<int2> oc;
+        o8.setup((uchar4*)rgba8, npx, s);
+        of.setup((double4*)rgba_f64, rgba_f64 ? npx : 0, s);
+        oc.setup((int2*)px_counts, px_counts ? npx : 0, s);
+        A->out8 = o8.dev;
+        A->outf = of.dev;
+        A->outcnt = oc.dev;
+        unsigned long long* dstats = nullptr;
+        if (stats || count_bytes) {
+            XB_CUDA(cudaMallocAsync((void**)&dstats, 3 * sizeof(unsigned long long), s));
+            XB_CUDA(cudaMemsetAsync(dstats, 0, 3 * sizeof(unsigned long long), s));
+        }
+        A->stats = dstats;
+        xb::launch_render(*A, n_local, count_bytes != 0, s);
+        o8.finish();
+        of.finish();
+        oc.finish();
+        unsigned long long hs[3] = {0, 0, 0};
+        if (dstats) {
+            XB_CUDA(cudaMemcpyAsync(hs, dstats, sizeof hs, cudaMemcpyDeviceToHost, s));
+            XB_CUDA(cudaFreeAsync(dstats, s));
+        }
+        const bool host_out = o8.owned || of.owned || oc.owned || dstats;
+        if (host_out) XB_CUDA(cudaStreamSynchronize(s));
+        if (stats) {
+            stats[0] = (int64_t)hs[0];
+            stats[1] = (int64_t)hs[1];
+            stats[2] = (int64_t)hs[2];
+        }
+    });
+}
+
+int xb_unpack_tiles(const void* packed, int64_t tiles_per_rank, int32_t world, int32_t width, int32_t height,
+                    void* rgba8, void* stream) {
+    return guarded([&] {
+        XB_CHECK(packed && rgba8 && world >= 1, XB_ERR_ARG, "bad unpack arguments");
+        const int tx = (width + xb::kTileW - 1) / xb::kTileW, ty = (height + xb::kTileH - 1) / xb::kTileH;
+        xb::launch_unpack((const uchar4*)packed, tiles_per_rank, world, tx, ty, width, height, (uchar4*)rgba8,
+                          (cudaStream_t)stream);
+    });
+}
+
+static int run_rays(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* act, const xb_march* mp,
+                    int mode, int64_t n, const double* o, const double* d, const double* t0, const double* t1,
+                    const double* rho, double* out, int64_t* counts) {
+    return guarded([&] {
+        XB_CHECK(mp && n >= 0, XB_ERR_ARG, "bad ray batch");
+        xb::DeviceGuard g(m->m.device);
+        OwnedStream st;
+        auto B = std::make_unique<xb::RayBatchArgs>();
+        B->S = scene_view(m, r, field);
+        check_active(act, r, mode == 0 ? "volume" : "iso");
+        B->vflags = act->a.flags.p;
+        B->iflags = act->a.flags.p;
+        fill_march(B->M, mp);
+        B->mode = mode;
+        B->n = n;
+        std::memcpy(B->tf, mp->tf_rgba, sizeof(B->tf));
+        xb::DevBuf<double> dO, dD, d0, d1, dr, dout;
+        xb::DevBuf<int64_t> dc;
+        dO.upload(o, 3 * n, st.s);
+        dD.upload(d, 3 * n, st.s);
+        d0.upload(t0, n, st.s);
+        d1.upload(t1, n, st.s);
+        dr.upload(rho, n, st.s);
+        dout.alloc(4 * n + 1);
+        dc.alloc(2 * n + 1);
+        B->o = dO.p; B->d = dD.p; B->t0 = d0.p; B->t1 = d1.p; B->rho = dr.p; B->out = dout.p; B->counts = dc.p;
+        xb::launch_rays(*B, st.s);
+        dout.download(out, 4 * n, st.s);
+        dc.download(counts, 2 * n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int xb_integrate_rays(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* vol,
+                      const xb_march* mp, int64_t n, const double* o, const double* d, const double* t0,
+                      const double* t1, const double* rho, double* out, int64_t* counts) {
+    return run_rays(m, r, field, vol, mp, 0, n, o, d, t0, t1, rho, out, counts);
+}
+
+int xb_iso_rays(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* iso, const xb_march* mp,
+                int64_t n, const double* o, const double* d, const double* t0, const double* t1, const double* rho,
+                double* out, int32_t* hit) {
+    std::vector<int64_t> c(2 * std::max<int64_t>(n, 1));
+    int rc = run_rays(m, r, field, iso, mp, 1, n, o, d, t0, t1, rho, out, c.data());
+    if (rc == XB_OK)
+        for (int64_t q = 0; q < n; q++) hit[q] = (int32_t)c[2 * q];
+    return rc;
+}
+
+int xb_sample_points(const xb_model* m, const xb_regions* r, int32_t field, int64_t n, const double* p,
+                     const int32_t* region, int32_t want_grad, int32_t* region_out, double* acc) {
+    return guarded([&] {
+        XB_CHECK(n >= 0, XB_ERR_ARG, "bad point count");
+        xb::DeviceGuard g(m->m.device);
+        OwnedStream st;
+        const xb::SceneView S = scene_view(m, r, field);
+        xb::DevBuf<double> dp, dacc;
+        xb::DevBuf<int32_t> drin, drout;
+        dp.upload(p, 3 * n, st.s);
+        if (region) drin.upload(region, n, st.s);
+        drout.alloc(n + 1);
+        dacc.alloc(9 * n + 1);
+        xb::sample_points(S, n, dp.p, region ? drin.p : nullptr, want_grad, drout.p, dacc.p, st.s);
+        drout.download(region_out, n, st.s);
+        dacc.download(acc, 9 * n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int xb_sample_scan(const xb_model* m, int32_t field, int64_t n, const double* p, double* out) {
+    return guarded([&] {
+        XB_CHECK(m && n >= 0, XB_ERR_ARG, "bad arguments");
+        XB_CHECK(field >= 0 && field < m->m.n_fields, XB_ERR_ARG, "field index out of range");
+        xb::DeviceGuard g(m->m.device);
+        OwnedStream st;
+        xb::SceneView S{};
+        S.brick_a = m->m.brick_a.p;
+        S.brick_m = m->m.brick_m.p;
+        S.vals = m->m.vals.p + (size_t)field * (size_t)m->m.n_cells;
+        xb::DevBuf<double> dp, dout;
+        dp.upload(p, 3 * n, st.s);
+        dout.alloc(2 * n + 1);
+        xb::sample_scan(S, m->m.n_bricks, n, dp.p, dout.p, st.s);
+        dout.download(out, 2 * n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int xb_trace_intervals(const xb_model* m, const xb_regions* r, const xb_active* a, int64_t n, const double* o,
+                       const double* d, double t_start, double t_max, int32_t cap, double* t_in, double* t_out,
+                       int32_t* region, int32_t* count) {
+    return guarded([&] {
+        XB_CHECK(n >= 0 && cap >= 0, XB_ERR_ARG, "bad trace arguments");
+        xb::DeviceGuard g(m->m.device);
+        OwnedStream st;
+        const xb::SceneView S = scene_view(m, r, 0);
+        check_active(a, r, "trace");
+        xb::DevBuf<double> dO, dD, di, dq;
+        xb::DevBuf<int32_t> dr, dc;
+        dO.upload(o, 3 * n, st.s);
+        dD.upload(d, 3 * n, st.s);
+        di.alloc((size_t)n * cap + 1);
+        dq.alloc((size_t)n * cap + 1);
+        dr.alloc((size_t)n * cap + 1);
+        dc.alloc(n + 1);
+        xb::trace_intervals(S, a->a.flags.p, n, dO.p, dD.p, t_start, t_max, cap, di.p, dq.p, dr.p, dc.p, st.s);
+        di.download(t_in, (size_t)n * cap, st.s);
+        dq.download(t_out, (size_t)n * cap, st.s);
+        dr.download(region, (size_t)n * cap, st.s);
+        dc.download(count, n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,531 @@
+// march.cuh — device functions of the fused ray-march (paper §4, §5).
+//
+// Everything here restates the reference's FP64 arithmetic operation for
+// operation (R/render.py, R/accel.py, R/sampling.py; R/ =
+// /root/reference/pkg/src/amrvol/).  The library is compiled with
+// -fmad=false so no multiply-add is contracted, like numba's LLVM code.
+//
+// Region traversal.  The reference finds every next region with a fresh
+// closest-hit BVH query from the root, t_start = t_out + eps
+// (R/render.py:394-397, R/accel.py:285-352).  Because regions are disjoint
+// axis-aligned boxes, their numeric slab intervals [r_in, r_out) are pairwise
+// disjoint (slab t's are monotone in the box bounds under IEEE rounding), so
+// the closest-hit answer for t_start is simply the first non-empty interval,
+// in r_in order, that is not entirely before t_start.  The ABR build is a k-d
+// split, so a front-to-back walk of that k-d tree enumerates regions in
+// exactly r_in order; culling uses the same monotone arithmetic, so it never
+// drops a region the reference would return.  One walk per ray replaces one
+// root-to-leaf descent per region visit.
+#pragma once
+#include "common.cuh"
+
+namespace xb {
+
+constexpr double kEpsWeight = 1e-12;     // EPS_WEIGHT, R/sampling.py:37
+constexpr double kTFar = 1.0e30;         // _T_FAR, R/render.py:49
+constexpr int kKdStack = 64;
+
+// exact power of two for |e| < 1022 (brick cell widths, finest widths)
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
+
+struct Ray {
+    double o[3], d[3], inv[3];
+};
+
+__device__ __forceinline__ double rho_hash(uint64_t pixel, uint64_t seed) {
+    // _rho_hash, R/render.py:226-233
+    uint64_t z = pixel ^ seed;
+    z = z + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+__device__ __forceinline__ double restart_t(double t_out) {
+    // _restart, R/render.py:257-260
+    double e = 1e-7 * t_out;
+    return t_out + (e > 1e-7 ? e : 1e-7);
+}
+
+// _slab, R/accel.py:254-282, on a half-unit integer box (values * 0.5 exact).
+// 1/d is hoisted per ray: the reference recomputes the same rounded quotient.
+__device__ __forceinline__ void slab_h(const int32_t* lo_h, const int32_t* hi_h, const Ray& r, double& tmin_o,
+                                       double& tmax_o) {
+    double tmin = -INFINITY, tmax = INFINITY;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        double lo = (double)lo_h[a] * 0.5, hi = (double)hi_h[a] * 0.5;
+        if (r.d[a] == 0.0) {
+            if (r.o[a] < lo || r.o[a] >= hi) { tmin_o = INFINITY; tmax_o = -INFINITY; return; }
+        } else {
+            double t0 = (lo - r.o[a]) * r.inv[a], t1 = (hi - r.o[a]) * r.inv[a];
+            if (t0 > t1) { double t = t0; t0 = t1; t1 = t; }
+            if (t0 > tmin) tmin = t0;
+            if (t1 < tmax) tmax = t1;
+            if (tmin > tmax) { tmin_o = INFINITY; tmax_o = -INFINITY; return; }
+        }
+    }
+    tmin_o = tmin;
+    tmax_o = tmax;
+}
+
+struct SceneView {
+    const int4* __restrict__ brick_a;
+    const uint32_t* __restrict__ brick_m;
+    const float* __restrict__ vals;
+    const RegionRec* __restrict__ rec;
+    const int32_t* __restrict__ rids;
+    const KdNode* __restrict__ kd;
+    int32_t root_lo[3], root_hi[3];
+    int64_t n_kd;
+};
+
+// ---------------------------------------------------------------------------
+// ordered k-d walk (see header comment)
+
+struct KdWalk {
+    int node;          // current node, -1: pop next
+    double tn, tf;     // every region below `node` has tn <= r_in, r_out <= tf
+    int sp;
+    int st_node[kKdStack];
+    float st_tn[kKdStack], st_tf[kKdStack];  // conservative (tn rounded down, tf up)
+};
+
+__device__ __forceinline__ void kd_begin(const SceneView& S, const Ray& r, KdWalk& w) {
+    double a, b;
+    slab_h(S.root_lo, S.root_hi, r, a, b);
+    w.sp = 0;
+    if (S.n_kd == 0 || !(a <= b)) { w.node = -2; return; }  // ray misses every region
+    w.node = 0;
+    w.tn = a;
+    w.tf = b;
+}
+
+// Next region whose interval is non-empty after clipping to [t, tmax] —
+// exactly `_bvh_next_hit(t, tmax)` over the regions with flags set.
+__device__ __forceinline__ bool kd_next(const SceneView& S, const uint8_t* __restrict__ flags, const Ray& r, KdWalk& w,
+                                        double t, double tmax, int& rid, double& c_in, double& c_out) {
+    if (w.node == -2) return false;
+    for (;;) {
+        if (w.node < 0) {
+            bool got = false;
+            while (w.sp > 0) {
+                --w.sp;
+                double tf = (double)w.st_tf[w.sp], tn = (double)w.st_tn[w.sp];
+                if (tf <= t || tn >= tmax) continue;
+                w.node = w.st_node[w.sp];
+                w.tn = tn;
+                w.tf = tf;
+                got = true;
+                break;
+            }
+            if (!got) { w.node = -2; return false; }
+        }
+        const int node = w.node;
+        if (!flags[node] || w.tf <= t || w.tn >= tmax) { w.node = -1; continue; }
+        const KdNode nd = S.kd[node];
+        if ((nd.a & 3) != 3) {  // interior (cavity leaves never have a set flag)
+            const int axis = nd.a & 3, left = nd.a >> 2;
+            const double p = (double)nd.b * 0.5;
+            if (r.d[axis] == 0.0) {  // half-open rule: only the side containing o
+                w.node = r.o[axis] < p ? left : left + 1;
+                continue;
+            }
+            const double tp = (p - r.o[axis]) * r.inv[axis];
+            const int near_c = r.d[axis] > 0.0 ? left : left + 1;
+            const int far_c = near_c == left ? left + 1 : left;
+            if (tp >= w.tf) { w.node = near_c; continue; }      // far side: r_in >= tp >= tf
+            if (tp <= w.tn) { w.node = far_c; continue; }       // near side: r_out <= tp <= tn
+            if (tp < tmax && w.sp < kKdStack) {
+                w.st_node[w.sp] = far_c;
+                w.st_tn[w.sp] = __double2float_rd(tp);
+                w.st_tf[w.sp] = __double2float_ru(w.tf);
+                w.sp++;
+            } else if (tp < tmax) {
+                __trap();  // tree deeper than the stack: rejected at scene setup
+            }
+            w.node = near_c;
+            w.tf = tp;
+            continue;
+        }
+        // leaf with an active region
+        w.node = -1;
+        const int reg = nd.a >> 2;
+        const RegionRec rr = S.rec[reg];
+        double r_in, r_out;
+        slab_h(rr.lo, rr.hi, r, r_in, r_out);
+        double ci = r_in > t ? r_in : t;
+        double co = r_out < tmax ? r_out : tmax;
+        if (ci < co) {
+            rid = reg;
+            c_in = ci;
+            c_out = co;
+            return true;
+        }
+    }
+}
+
+// half-open point location through the k-d tree (`_bvh_point_query` on the
+// all-regions index, R/accel.py:355-388)
+__device__ __forceinline__ int kd_point(const SceneView& S, double px, double py, double pz) {
+    if (S.n_kd == 0) return -1;
+    const double p[3] = {px, py, pz};
+    int node = 0;
+    for (;;) {
+        const KdNode nd = S.kd[node];
+        if (nd.a == -1) return -1;
+        if ((nd.a & 3) == 3) {
+            const int reg = nd.a >> 2;
+            const RegionRec rr = S.rec[reg];
+#pragma unroll
+            for (int a = 0; a < 3; a++)
+                if (!(p[a] >= (double)rr.lo[a] * 0.5 && p[a] < (double)rr.hi[a] * 0.5)) return -1;
+            return reg;
+        }
+        const int axis = nd.a & 3, left = nd.a >> 2;
+        node = p[axis] < (double)nd.b * 0.5 ? left : left + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// reconstruction: _accumulate_bricks / _gradient_bricks fused in one gather
+// (R/sampling.py:57-103, 123-181).  GRAD=false: value only.
+
+struct Accum {
+    double num, den;              // unshifted (value path)
+    double gnum, dn[3], dd[3];    // v0-shifted (gradient path)
+    double v0;
+    bool have_ref;
+    int64_t n_nz;                 // cells with h > 0 (byte accounting)
+};
+
+template <bool GRAD>
+__device__ __forceinline__ void gather(const SceneView& S, const int32_t* __restrict__ ids, int nids, double px,
+                                       double py, double pz, Accum& A) {
+    A.num = 0.0; A.den = 0.0;
+    if (GRAD) {
+        A.gnum = 0.0;
+        A.dn[0] = A.dn[1] = A.dn[2] = 0.0;
+        A.dd[0] = A.dd[1] = A.dd[2] = 0.0;
+        A.v0 = 0.0;
+        A.have_ref = false;
+    }
+    A.n_nz = 0;
+    for (int t = 0; t < nids; t++) {
+        const int b = __ldg(ids + t);
+        const int4 ba = __ldg(S.brick_a + b);
+        const uint32_t bm = __ldg(S.brick_m + b);
+        const int lev = bm & 31;
+        const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
+        const double w = pow2(lev), iw_d = pow2(-lev);
+        const int64_t iw = (int64_t)1 << lev;
+        const int64_t lx = ba.x, ly = ba.y, lz = ba.z;
+        // floor((p - l) / w - 0.5): division by a power of two == scaling
+        const int64_t x0 = (int64_t)floor((px - (double)lx) * iw_d - 0.5);
+        const int64_t y0 = (int64_t)floor((py - (double)ly) * iw_d - 0.5);
+        const int64_t z0 = (int64_t)floor((pz - (double)lz) * iw_d - 0.5);
+        const int64_t xs = x0 > 0 ? x0 : 0, xe = x0 + 2 < nx ? x0 + 2 : nx;
+        const int64_t ys = y0 > 0 ? y0 : 0, ye = y0 + 2 < ny ? y0 + 2 : ny;
+        const int64_t zs = z0 > 0 ? z0 : 0, ze = z0 + 2 < nz ? z0 + 2 : nz;
+        const float* __restrict__ base = S.vals + (uint32_t)ba.w;
+        for (int64_t z = zs; z < ze; z++) {
+            const double ck = (double)(lz + z * iw) + 0.5 * w;
+            const double hz = 1.0 - fabs(ck - pz) * iw_d;
+            for (int64_t y = ys; y < ye; y++) {
+                const double cj = (double)(ly + y * iw) + 0.5 * w;
+                const double hy = 1.0 - fabs(cj - py) * iw_d;
+                for (int64_t x = xs; x < xe; x++) {
+                    const double ci = (double)(lx + x * iw) + 0.5 * w;
+                    const double hx = 1.0 - fabs(ci - px) * iw_d;
+                    if (hx > 0.0 && hy > 0.0 && hz > 0.0) {
+                        const double h = hx * hy * hz;
+                        const double v = (double)__ldg(base + x + nx * (y + ny * z));
+                        A.num += h * v;
+                        A.den += h;
+                        A.n_nz++;
+                        if (GRAD) {
+                            const double sx = ci - px > 0.0 ? 1.0 : -1.0;
+                            const double sy = cj - py > 0.0 ? 1.0 : -1.0;
+                            const double sz = ck - pz > 0.0 ? 1.0 : -1.0;
+                            const double gx = sx * iw_d * hy * hz;
+                            const double gy = sy * iw_d * hx * hz;
+                            const double gz = sz * iw_d * hx * hy;
+                            if (!A.have_ref) { A.v0 = v; A.have_ref = true; }
+                            const double u = v - A.v0;
+                            A.gnum += h * u;
+                            A.dn[0] += gx * u; A.dn[1] += gy * u; A.dn[2] += gz * u;
+                            A.dd[0] += gx; A.dd[1] += gy; A.dd[2] += gz;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void analytic_gradient(const Accum& A, double g[3]) {
+    // _sample_gradient mode 1, R/render.py:295-306
+    if (A.den <= kEpsWeight) { g[0] = g[1] = g[2] = 0.0; return; }
+    const double d2 = A.den * A.den;
+#pragma unroll
+    for (int a = 0; a < 3; a++) g[a] = (A.dn[a] * A.den - A.gnum * A.dd[a]) / d2;
+}
+
+__device__ __forceinline__ double shade_factor(const double g[3], const Ray& r) {
+    // _shade_factor, R/render.py:284-289
+    const double n = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    if (n == 0.0) return 0.2;
+    return 0.2 + 0.8 * fabs(g[0] * r.d[0] + g[1] * r.d[1] + g[2] * r.d[2]) / n;
+}
+
+__device__ __forceinline__ void tf_eval(const double* tf, double tf_lo, double tf_hi, double v, double c[4]) {
+    // _tf_eval, R/render.py:236-254
+    double t = (v - tf_lo) / (tf_hi - tf_lo);
+    if (t < 0.0) t = 0.0;
+    else if (t > 1.0) t = 1.0;
+    const double x = t * 255.0;
+    const int i = (int)x;
+    if (i >= 255) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) c[k] = tf[255 * 4 + k];
+        return;
+    }
+    const double f = x - (double)i, g = 1.0 - f;
+#pragma unroll
+    for (int k = 0; k < 4; k++) c[k] = g * tf[i * 4 + k] + f * tf[(i + 1) * 4 + k];
+}
+
+// central / clamped-central gradient (R/render.py:307-376)
+__device__ inline void central_gradient(const SceneView& S, int mode, double px, double py, double pz, int rid,
+                                        const int32_t* ids, int nids, double val, double g[3], int64_t* n_evals) {
+    const RegionRec rr = S.rec[rid];
+    const double h = 0.5 * pow2(rr.meta >> 24);
+    const double p[3] = {px, py, pz};
+    g[0] = g[1] = g[2] = 0.0;
+    Accum A;
+    for (int a = 0; a < 3; a++) {
+        double qp[3] = {px, py, pz}, qm[3] = {px, py, pz};
+        qp[a] = p[a] + h;
+        qm[a] = p[a] - h;
+        if (mode == 3) {
+            for (int c = 0; c < 3; c++) {
+                const double lo = (double)rr.lo[c] * 0.5, hi = (double)rr.hi[c] * 0.5;
+                qp[c] = fmin(fmax(qp[c], lo), hi);
+                qm[c] = fmin(fmax(qm[c], lo), hi);
+            }
+            gather<false>(S, ids, nids, qp[0], qp[1], qp[2], A);
+            const double np_ = A.num, dp = A.den;
+            gather<false>(S, ids, nids, qm[0], qm[1], qm[2], A);
+            const double nm = A.num, dm = A.den;
+            *n_evals += 2;
+            if (dp > kEpsWeight && dm > kEpsWeight) {
+                const double span = qp[a] - qm[a];
+                if (span > 0.0) g[a] = (np_ / dp - nm / dm) / span;
+            }
+        } else {
+            double fp = 0.0, fm = 0.0;
+            bool okp = false, okm = false;
+            const int rp = kd_point(S, qp[0], qp[1], qp[2]);
+            if (rp >= 0) {
+                const RegionRec q = S.rec[rp];
+                gather<false>(S, S.rids + q.ids_begin, q.meta & 0xffffff, qp[0], qp[1], qp[2], A);
+                *n_evals += 1;
+                if (A.den > kEpsWeight) { fp = A.num / A.den; okp = true; }
+            }
+            const int rm = kd_point(S, qm[0], qm[1], qm[2]);
+            if (rm >= 0) {
+                const RegionRec q = S.rec[rm];
+                gather<false>(S, S.rids + q.ids_begin, q.meta & 0xffffff, qm[0], qm[1], qm[2], A);
+                *n_evals += 1;
+                if (A.den > kEpsWeight) { fm = A.num / A.den; okm = true; }
+            }
+            double gg;
+            if (okp && okm) gg = (fp - fm) / (2.0 * h);
+            else if (okp) gg = (fp - val) / h;
+            else if (okm) gg = (val - fm) / h;
+            else gg = 0.0;
+            g[a] = gg;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// per-ray march state shared by the frame and ray-batch kernels
+
+struct MarchConst {
+    double spc, rate, early;
+    uint64_t seed;
+    int grad_mode;
+    int n_planes;
+    double planes[6][4];
+    int iso_on;
+    double iso_value;
+    double iso_rgb[3];
+    double tf_lo, tf_hi;
+};
+
+struct RayStats {
+    int64_t regions, samples, bytes;
+};
+
+__device__ __forceinline__ void clip_ray(const MarchConst& M, const Ray& r, double& tmin, double& tmax) {
+    // _clip_ray, R/render.py:263-281
+    for (int i = 0; i < M.n_planes; i++) {
+        const double* pl = M.planes[i];
+        const double nd = pl[0] * r.d[0] + pl[1] * r.d[1] + pl[2] * r.d[2];
+        const double no = pl[0] * r.o[0] + pl[1] * r.o[1] + pl[2] * r.o[2];
+        if (nd > 0.0) {
+            const double t = (pl[3] - no) / nd;
+            if (t < tmax) tmax = t;
+        } else if (nd < 0.0) {
+            const double t = (pl[3] - no) / nd;
+            if (t > tmin) tmin = t;
+        } else if (no > pl[3]) {
+            tmin = 1.0;
+            tmax = 0.0;
+            return;
+        }
+    }
+}
+
+template <bool COUNT>
+__device__ __forceinline__ void count_eval(RayStats& st, int nids, const Accum& A) {
+    if (COUNT) st.bytes += 16 * (int64_t)nids + 4 * A.n_nz;
+}
+
+// _iso_ray, R/render.py:456-518
+template <bool COUNT>
+__device__ bool iso_ray(const SceneView& S, const uint8_t* __restrict__ iflags, const MarchConst& M, const Ray& r,
+                        double tmin, double tmax, double rho, double& t_hit, double g[3], RayStats& st) {
+    KdWalk w;
+    kd_begin(S, r, w);
+    double t = tmin;
+    const double iso = M.iso_value;
+    g[0] = g[1] = g[2] = 0.0;
+    Accum A;
+    for (;;) {
+        int rid;
+        double t_in, t_out;
+        if (!kd_next(S, iflags, r, w, t, tmax, rid, t_in, t_out)) return false;
+        const RegionRec rr = S.rec[rid];
+        const int nids = rr.meta & 0xffffff;
+        const int32_t* ids = S.rids + rr.ids_begin;
+        if (COUNT) st.bytes += 32 + 4 * (int64_t)nids;
+        const double fw = pow2(rr.meta >> 24);
+        const double dt = fw / (M.spc * M.rate);
+        double prev_t = t_in;
+        gather<false>(S, ids, nids, r.o[0] + t_in * r.d[0], r.o[1] + t_in * r.d[1], r.o[2] + t_in * r.d[2], A);
+        count_eval<COUNT>(st, nids, A);
+        bool prev_ok = A.den > kEpsWeight;
+        double prev_f = prev_ok ? A.num / A.den - iso : 0.0;
+        double k = floor(t_in / dt - rho) + 1.0;
+        bool done = false;
+        while (!done) {
+            double tk = dt * (k + rho);
+            k += 1.0;
+            if (tk >= t_out) { tk = t_out; done = true; }
+            else if (tk <= prev_t) continue;
+            gather<false>(S, ids, nids, r.o[0] + tk * r.d[0], r.o[1] + tk * r.d[1], r.o[2] + tk * r.d[2], A);
+            count_eval<COUNT>(st, nids, A);
+            const bool ok = A.den > kEpsWeight;
+            const double f = ok ? A.num / A.den - iso : 0.0;
+            if (prev_ok && ok && ((prev_f <= 0.0 && f >= 0.0) || (prev_f >= 0.0 && f <= 0.0)) &&
+                !(prev_f == 0.0 && f == 0.0)) {
+                double lo_t = prev_t, hi_t = tk, flo = prev_f;
+                for (int it = 0; it < 16; it++) {
+                    const double mid = 0.5 * (lo_t + hi_t);
+                    gather<false>(S, ids, nids, r.o[0] + mid * r.d[0], r.o[1] + mid * r.d[1], r.o[2] + mid * r.d[2], A);
+                    count_eval<COUNT>(st, nids, A);
+                    const double fm = A.den > kEpsWeight ? A.num / A.den - iso : 0.0;
+                    if ((flo <= 0.0 && fm <= 0.0) || (flo >= 0.0 && fm >= 0.0)) { lo_t = mid; flo = fm; }
+                    else hi_t = mid;
+                }
+                t_hit = 0.5 * (lo_t + hi_t);
+                gather<true>(S, ids, nids, r.o[0] + t_hit * r.d[0], r.o[1] + t_hit * r.d[1], r.o[2] + t_hit * r.d[2], A);
+                if (A.den > kEpsWeight) {
+                    const double d2 = A.den * A.den;
+                    for (int a = 0; a < 3; a++) g[a] = (A.dn[a] * A.den - A.gnum * A.dd[a]) / d2;
+                }
+                return true;
+            }
+            prev_t = tk;
+            prev_f = f;
+            prev_ok = ok;
+        }
+        t = restart_t(t_out);
+        if (t >= tmax) return false;
+    }
+}
+
+// _volume_ray, R/render.py:380-453.  GRAD: 0 none, 1 analytic (fused gather),
+// 2 central / 3 clamped central (mode in M.grad_mode).
+template <int GRAD, bool COUNT>
+__device__ void volume_ray(const SceneView& S, const uint8_t* __restrict__ vflags, const MarchConst& M,
+                           const double* tf, const Ray& r, double tmin, double tmax, double rho, double acc[4],
+                           RayStats& st) {
+    double ar = 0.0, ag = 0.0, ab = 0.0, aa = 0.0;
+    KdWalk w;
+    kd_begin(S, r, w);
+    double t = tmin;
+    Accum A;
+    while (aa < M.early) {
+        int rid;
+        double t_in, t_out;
+        if (!kd_next(S, vflags, r, w, t, tmax, rid, t_in, t_out)) break;
+        st.regions++;
+        const RegionRec rr = S.rec[rid];
+        const int nids = rr.meta & 0xffffff;
+        const int32_t* ids = S.rids + rr.ids_begin;
+        if (COUNT) st.bytes += 32 + 4 * (int64_t)nids;
+        const double fw = pow2(rr.meta >> 24);
+        const double dt = fw / (M.spc * M.rate);
+        const double s1 = fw / M.spc;
+        double prev = t_in;
+        double k = floor(t_in / dt - rho) + 1.0;
+        bool done = false;
+        while (!done) {
+            double tk = dt * (k + rho);
+            k += 1.0;
+            if (tk >= t_out) { tk = t_out; done = true; }
+            else if (tk <= prev) continue;
+            const double sl = tk - prev;
+            const double mid = 0.5 * (prev + tk);
+            prev = tk;
+            st.samples++;
+            const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1], pz = r.o[2] + mid * r.d[2];
+            gather<GRAD == 1>(S, ids, nids, px, py, pz, A);
+            count_eval<COUNT>(st, nids, A);
+            if (A.den > kEpsWeight) {
+                const double v = A.num / A.den;
+                double c[4];
+                tf_eval(tf, M.tf_lo, M.tf_hi, v, c);
+                if (c[3] > 0.0) {
+                    const double alpha = 1.0 - pow(1.0 - c[3], sl / s1);
+                    if (GRAD != 0) {
+                        double g[3];
+                        if (GRAD == 1) {
+                            analytic_gradient(A, g);
+                        } else {
+                            int64_t ne = 0;
+                            central_gradient(S, M.grad_mode, px, py, pz, rid, ids, nids, v, g, &ne);
+                        }
+                        const double f = shade_factor(g, r);
+                        c[0] *= f; c[1] *= f; c[2] *= f;
+                    }
+                    const double wgt = alpha * (1.0 - aa);
+                    ar += wgt * c[0];
+                    ag += wgt * c[1];
+                    ab += wgt * c[2];
+                    aa += wgt;
+                    if (aa >= M.early) break;
+                }
+            }
+        }
+        t = restart_t(t_out);
+        if (t >= tmax) break;
+    }
+    acc[0] = ar; acc[1] = ag; acc[2] = ab; acc[3] = aa;
+}
+
+}  // namespace xb

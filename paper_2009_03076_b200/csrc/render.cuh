@@ -1,0 +1,45 @@
+// render.cuh — kernel parameter blocks for the march kernels.
+#pragma once
+#include "march.cuh"
+
+namespace xb {
+
+constexpr int kTileW = 16, kTileH = 8;  // one CUDA block = one screen tile
+
+// Passed by value as a __grid_constant__ kernel parameter (~8.6 KB < 32 KB):
+// the call needs no device allocation, so concurrent renders are reentrant.
+struct RenderArgs {
+    SceneView S;
+    const uint8_t* vflags;  // per k-d node: subtree holds an active volume region
+    const uint8_t* iflags;  // same for the iso predicate
+    MarchConst M;
+    int W, H;
+    double pos[3], right[3], up[3], fwd[3];
+    double tan_half, aspect;
+    int tiles_x, tiles_y, tile_rank, tile_world, packed;
+    uchar4* out8;
+    double4* outf;
+    int2* outcnt;
+    unsigned long long* stats;  // [regions, samples, algorithmic bytes]
+    double tf[1024];
+};
+
+struct RayBatchArgs {
+    SceneView S;
+    const uint8_t* vflags;
+    const uint8_t* iflags;
+    MarchConst M;
+    int mode;  // 0 volume (integrate_ray), 1 iso (iso_intersect)
+    int64_t n;
+    const double *o, *d, *t0, *t1, *rho;
+    double* out;       // (n,4): RGBA, or (t_hit, gx, gy, gz)
+    int64_t* counts;   // (n,2): regions, samples  | hit flag
+    double tf[1024];
+};
+
+void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaStream_t s);
+void launch_rays(const RayBatchArgs& B, cudaStream_t s);
+void launch_unpack(const uchar4* packed, int64_t tiles_per_rank, int world, int tiles_x, int tiles_y, int W, int H,
+                   uchar4* img, cudaStream_t s);
+
+}  // namespace xb
