@@ -213,7 +213,7 @@ __device__ __forceinline__ void gather(const SceneView& S, const int32_t* __rest
     }
     A.n_nz = 0;
     for (int t = 0; t < nids; t++) {
-        const int b = __ldg(ids + t);
+        const int b = ids[t];  // plain load: callers may pass a local id
         const int4 ba = __ldg(S.brick_a + b);
         const uint32_t bm = __ldg(S.brick_m + b);
         const int lev = bm & 31;
