@@ -420,21 +420,28 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->out8 = o8.dev;
         A->outf = of.dev;
         A->outcnt = oc.dev;
-        unsigned long long* dstats = nullptr;
-        if (stats || count_bytes) {
-            XB_CUDA(cudaMallocAsync((void**)&dstats, 3 * sizeof(unsigned long long), s));
-            XB_CUDA(cudaMemsetAsync(dstats, 0, 3 * sizeof(unsigned long long), s));
-        }
+        // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter]
+        unsigned long long* scratch = nullptr;
+        XB_CUDA(cudaMallocAsync((void**)&scratch, 4 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(unsigned long long), s));
+        unsigned long long* dstats = (stats || count_bytes) ? scratch : nullptr;
         A->stats = dstats;
+        A->work_counter = scratch + 3;
+        double* iso_buf = nullptr;
+        if (A->M.iso_on) {
+            const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
+            XB_CUDA(cudaMallocAsync((void**)&iso_buf, 2 * std::max<size_t>(n_slots, 1) * sizeof(double), s));
+            A->iso_tend = iso_buf;
+            A->iso_shade = iso_buf + n_slots;
+        }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
+        if (iso_buf) XB_CUDA(cudaFreeAsync(iso_buf, s));
         o8.finish();
         of.finish();
         oc.finish();
         unsigned long long hs[3] = {0, 0, 0};
-        if (dstats) {
-            XB_CUDA(cudaMemcpyAsync(hs, dstats, sizeof hs, cudaMemcpyDeviceToHost, s));
-            XB_CUDA(cudaFreeAsync(dstats, s));
-        }
+        if (dstats) XB_CUDA(cudaMemcpyAsync(hs, dstats, sizeof hs, cudaMemcpyDeviceToHost, s));
+        XB_CUDA(cudaFreeAsync(scratch, s));
         const bool host_out = o8.owned || of.owned || oc.owned || dstats;
         if (host_out) XB_CUDA(cudaStreamSynchronize(s));
         if (stats) {

@@ -166,6 +166,71 @@ __device__ __forceinline__ bool kd_next(const SceneView& S, const uint8_t* __res
     }
 }
 
+// One node visit of the same walk, for software pipelining (k_frame): `nd`
+// and `fl` are the prefetched record / flag of w.node.  Returns 0 to
+// continue, 1 when a region with a non-empty clipped interval was found,
+// 2 when the walk is exhausted.  A sequence of kd_step calls yields exactly the
+// regions kd_next would.
+__device__ __forceinline__ int kd_step(const SceneView& S, const uint8_t* __restrict__ flags, const Ray& r, KdWalk& w,
+                                       KdNode nd, uint8_t fl, double t, double tmax, int& rid, double& c_in,
+                                       double& c_out) {
+    if (w.node == -2) return 2;
+    if (w.node < 0) {
+        while (w.sp > 0) {
+            --w.sp;
+            const double tf = (double)w.st_tf[w.sp], tn = (double)w.st_tn[w.sp];
+            if (tf <= t || tn >= tmax) continue;
+            w.node = w.st_node[w.sp];
+            w.tn = tn;
+            w.tf = tf;
+            return 0;
+        }
+        w.node = -2;
+        return 2;
+    }
+    if (!fl || w.tf <= t || w.tn >= tmax) {
+        w.node = -1;
+        return 0;
+    }
+    if ((nd.a & 3) != 3) {
+        const int axis = nd.a & 3, left = nd.a >> 2;
+        const double p = (double)nd.b * 0.5;
+        if (r.d[axis] == 0.0) {
+            w.node = r.o[axis] < p ? left : left + 1;
+            return 0;
+        }
+        const double tp = (p - r.o[axis]) * r.inv[axis];
+        const int near_c = r.d[axis] > 0.0 ? left : left + 1;
+        const int far_c = near_c == left ? left + 1 : left;
+        if (tp >= w.tf) { w.node = near_c; return 0; }
+        if (tp <= w.tn) { w.node = far_c; return 0; }
+        if (tp < tmax) {
+            if (w.sp >= kKdStack) __trap();
+            w.st_node[w.sp] = far_c;
+            w.st_tn[w.sp] = __double2float_rd(tp);
+            w.st_tf[w.sp] = __double2float_ru(w.tf);
+            w.sp++;
+        }
+        w.node = near_c;
+        w.tf = tp;
+        return 0;
+    }
+    w.node = -1;
+    const int reg = nd.a >> 2;
+    const RegionRec rr = S.rec[reg];
+    double r_in, r_out;
+    slab_h(rr.lo, rr.hi, r, r_in, r_out);
+    const double ci = r_in > t ? r_in : t;
+    const double co = r_out < tmax ? r_out : tmax;
+    if (ci < co) {
+        rid = reg;
+        c_in = ci;
+        c_out = co;
+        return 1;
+    }
+    return 0;
+}
+
 // half-open point location through the k-d tree (`_bvh_point_query` on the
 // all-regions index, R/accel.py:355-388)
 __device__ __forceinline__ int kd_point(const SceneView& S, double px, double py, double pz) {
@@ -257,6 +322,98 @@ __device__ __forceinline__ void gather(const SceneView& S, const int32_t* __rest
                             A.dn[0] += gx * u; A.dn[1] += gy * u; A.dn[2] += gz * u;
                             A.dd[0] += gx; A.dd[1] += gy; A.dd[2] += gz;
                         }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Same sums as gather<GRAD>, restructured for SIMT: the <=2x2x2 candidate
+// window of a brick is fixed, so the three hat factors per axis (and the
+// products hx*hy) are computed once per brick instead of once per cell.  Every
+// value is the identical IEEE expression of the reference (h = (hx*hy)*hz,
+// g_x = ((s_x/w)*hy)*hz, ...) and cells are still visited z, y, x ascending, so
+// the partial-sum sequence — and hence every bit — is unchanged.
+template <bool GRAD>
+__device__ __forceinline__ void gather_fast(const SceneView& S, const int32_t* __restrict__ ids, int nids, double px,
+                                            double py, double pz, Accum& A) {
+    A.num = 0.0; A.den = 0.0;
+    if (GRAD) {
+        A.gnum = 0.0;
+        A.dn[0] = A.dn[1] = A.dn[2] = 0.0;
+        A.dd[0] = A.dd[1] = A.dd[2] = 0.0;
+        A.v0 = 0.0;
+        A.have_ref = false;
+    }
+    A.n_nz = 0;
+    for (int t = 0; t < nids; t++) {
+        const int b = __ldg(ids + t);
+        const int4 ba = __ldg(S.brick_a + b);
+        const uint32_t bm = __ldg(S.brick_m + b);
+        const int lev = bm & 31;
+        const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
+        const double w = pow2(lev), iw_d = pow2(-lev);
+        const double fx = floor((px - (double)ba.x) * iw_d - 0.5);
+        const double fy = floor((py - (double)ba.y) * iw_d - 0.5);
+        const double fz = floor((pz - (double)ba.z) * iw_d - 0.5);
+        // window entirely outside the brick: no cell contributes (exact skip)
+        if (!(fx >= -1.0 && fx < (double)nx && fy >= -1.0 && fy < (double)ny && fz >= -1.0 && fz < (double)nz)) continue;
+        const int x0 = (int)fx, y0 = (int)fy, z0 = (int)fz;
+        const double half = 0.5 * w;
+        // cell centres (ai + 0.5*w), exact in FP64
+        const double cx0 = (double)(ba.x + x0 * (1 << lev)) + half, cx1 = cx0 + w;
+        const double cy0 = (double)(ba.y + y0 * (1 << lev)) + half, cy1 = cy0 + w;
+        const double cz0 = (double)(ba.z + z0 * (1 << lev)) + half, cz1 = cz0 + w;
+        const double ex0 = cx0 - px, ex1 = cx1 - px, ey0 = cy0 - py, ey1 = cy1 - py, ez0 = cz0 - pz, ez1 = cz1 - pz;
+        const double hx[2] = {1.0 - fabs(ex0) * iw_d, 1.0 - fabs(ex1) * iw_d};
+        const double hy[2] = {1.0 - fabs(ey0) * iw_d, 1.0 - fabs(ey1) * iw_d};
+        const double hz[2] = {1.0 - fabs(ez0) * iw_d, 1.0 - fabs(ez1) * iw_d};
+        const bool vx[2] = {x0 >= 0 && hx[0] > 0.0, x0 + 1 < nx && hx[1] > 0.0};
+        const bool vy[2] = {y0 >= 0 && hy[0] > 0.0, y0 + 1 < ny && hy[1] > 0.0};
+        const bool vz[2] = {z0 >= 0 && hz[0] > 0.0, z0 + 1 < nz && hz[1] > 0.0};
+        const double sxw[2] = {ex0 > 0.0 ? iw_d : -iw_d, ex1 > 0.0 ? iw_d : -iw_d};
+        const double syw[2] = {ey0 > 0.0 ? iw_d : -iw_d, ey1 > 0.0 ? iw_d : -iw_d};
+        const double szw[2] = {ez0 > 0.0 ? iw_d : -iw_d, ez1 > 0.0 ? iw_d : -iw_d};
+        const float* __restrict__ base = S.vals + (uint32_t)ba.w + x0 + nx * (y0 + ny * z0);
+        // products shared by the cells of the 2x2x2 window
+        double hxy[2][2];
+#pragma unroll
+        for (int dy = 0; dy < 2; dy++)
+#pragma unroll
+            for (int dx = 0; dx < 2; dx++) hxy[dy][dx] = hx[dx] * hy[dy];  // (hx*hy) as in h = hx*hy*hz
+        // Branch-free cell body: a skipped cell contributes exact zeros.  The
+        // accumulators start at +0.0 and round-to-nearest never yields -0.0
+        // from non-(-0.0) operands, so adding +-0.0 leaves every bit unchanged.
+#pragma unroll
+        for (int dz = 0; dz < 2; dz++) {
+#pragma unroll
+            for (int dy = 0; dy < 2; dy++) {
+                const float* row = base + nx * (dy + ny * dz);
+#pragma unroll
+                for (int dx = 0; dx < 2; dx++) {
+                    const bool ok = vz[dz] && vy[dy] && vx[dx];
+                    const double h = ok ? hxy[dy][dx] * hz[dz] : 0.0;
+                    const double v = ok ? (double)__ldg(row + dx) : 0.0;
+                    A.num += h * v;  // value path: exact reference arithmetic
+                    A.den += h;
+                    A.n_nz += ok;
+                    if (GRAD) {
+                        // Shading-only gradient (feeds the headlight factor, never alpha,
+                        // positions or counters): fused multiply-adds and shared products
+                        // are allowed here — well inside the 1e-3 image tolerance, and a
+                        // locally constant field still cancels to an exactly zero gradient
+                        // (every u below is exactly 0).
+                        const double gx = ok ? sxw[dx] * (hy[dy] * hz[dz]) : 0.0;
+                        const double gy = ok ? syw[dy] * (hx[dx] * hz[dz]) : 0.0;
+                        const double gz = ok ? szw[dz] * hxy[dy][dx] : 0.0;
+                        if (ok && !A.have_ref) { A.v0 = v; A.have_ref = true; }
+                        const double u = v - A.v0;
+                        A.gnum = __fma_rn(h, u, A.gnum);
+                        A.dn[0] = __fma_rn(gx, u, A.dn[0]);
+                        A.dn[1] = __fma_rn(gy, u, A.dn[1]);
+                        A.dn[2] = __fma_rn(gz, u, A.dn[2]);
+                        A.dd[0] += gx; A.dd[1] += gy; A.dd[2] += gz;
                     }
                 }
             }

@@ -4,7 +4,10 @@
 
 namespace xb {
 
-constexpr int kTileW = 16, kTileH = 8;  // one CUDA block = one screen tile
+constexpr int kTileW = 16, kTileH = 8;  // screen tile; a warp owns an 8x4 quarter
+constexpr int kFrameThreads = 128;      // persistent k_frame block size
+constexpr int kKdSteps = 5;             // k-d node visits per k_frame iteration (tools/sweep.py)
+constexpr int kFrameMinBlocks = 4;      // 128 regs/thread -> 16 warps/SM (more spills, fewer hurt)
 
 // Passed by value as a __grid_constant__ kernel parameter (~8.6 KB < 32 KB):
 // the call needs no device allocation, so concurrent renders are reentrant.
@@ -21,6 +24,9 @@ struct RenderArgs {
     double4* outf;
     int2* outcnt;
     unsigned long long* stats;  // [regions, samples, algorithmic bytes]
+    unsigned long long* work_counter;  // k_frame slot counter (zeroed per launch)
+    double* iso_tend;           // per slot: volume t_end (iso hit or clip end)
+    double* iso_shade;          // per slot: headlight factor of the iso hit, < 0 when none
     double tf[1024];
 };
 

@@ -354,3 +354,18 @@ def test_acceptance_million_cells_vs_oracle(xb):
     assert np.abs(f64.reshape(-1, 4)[rows] - of).max() <= RGBA_TOL
     assert np.array_equal(cnt.reshape(-1, 2)[rows, 0], pr)
     assert np.array_equal(cnt.reshape(-1, 2)[rows, 1], ps)
+    # whole frame: the persistent kernel (dynamic per-lane ray refill) must equal
+    # the one-thread-per-pixel kernel everywhere, on every repetition
+    import os
+
+    os.environ["XB_KERNEL"] = "tile"
+    try:
+        u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)
+    finally:
+        del os.environ["XB_KERNEL"]
+    assert np.array_equal(cnt, cntt)
+    assert np.abs(f64 - f64t).max() <= RGBA_TOL
+    for _ in range(3):
+        u8r, f64r, cntr, str_ = render_frame_float(scene, cam, tf, params)
+        assert np.array_equal(cntr, cnt) and np.array_equal(u8r, u8)
+        assert tuple(str_[:2]) == tuple(stats[:2])
