@@ -1,4 +1,5 @@
 // abi.cu — extern "C" entry points of libexabricks (include/exabricks.h).
+#include <cmath>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -78,11 +79,13 @@ xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     S.rec = r->r.rec.p;
     S.rids = r->r.ids.p;
     S.kd = r->r.kd.p;
+    S.kd4 = r->r.kd4.p;
     for (int a = 0; a < 3; a++) {
         S.root_lo[a] = r->r.root_lo[a];
         S.root_hi[a] = r->r.root_hi[a];
     }
     S.n_kd = r->r.n_regions > 0 ? r->r.n_kd : 0;
+    S.n_kd4 = r->r.n_regions > 0 ? r->r.n_kd4 : 0;
     return S;
 }
 
@@ -102,6 +105,13 @@ void fill_march(xb::MarchConst& M, const xb_march* mp) {
     for (int c = 0; c < 3; c++) M.iso_rgb[c] = mp->iso_rgb[c];
     M.tf_lo = mp->tf_lo;
     M.tf_hi = mp->tf_hi;
+    M.tf_inv = 1.0 / (mp->tf_hi - mp->tf_lo);
+    for (int l = 0; l < 32; l++) {
+        const double fw = std::ldexp(1.0, l);
+        M.lv_dt[l] = fw / (M.spc * M.rate);
+        M.lv_s1[l] = fw / M.spc;
+        M.lv_is1[l] = 1.0 / M.lv_s1[l];
+    }
 }
 
 void check_active(const xb_active* a, const xb_regions* r, const char* what) {
@@ -388,6 +398,7 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->S = scene_view(m, r, field);
         check_active(vol, r, "volume");
         A->vflags = vol->a.flags.p;
+        A->vmask4 = vol->a.mask4.p;
         fill_march(A->M, mp);
         A->M.iso_on = (mp->iso_on && iso) ? 1 : 0;
         if (A->M.iso_on) check_active(iso, r, "iso");

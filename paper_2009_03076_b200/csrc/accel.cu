@@ -124,6 +124,7 @@ void build_active(const DevRegions& R, int kind, int field, double tf_lo, double
         if (m > 0) k_flags_level<<<grid_for(m, BS), BS, 0, s>>>(b, m, R.kd.p, out.act.p, out.flags.p);
     }
     check_launch("k_flags_level");
+    build_kd4_mask(R, out.flags.p, out.mask4, s);
     // active id list (ascending) for RegionBvh.prims / n_active
     CubTemp tmp;
     DevBuf<int32_t> a32(n + 1), pos(n + 1);

@@ -12,9 +12,13 @@ struct DevActive {
     int64_t n_active = 0;
     DevBuf<uint8_t> act;     // per region
     DevBuf<uint8_t> flags;   // per k-d node
+    DevBuf<uint8_t> mask4;   // per Kd4 node: active bit per child slot
     DevBuf<int32_t> prims;   // ascending active region ids
     double build_ms = 0.0;
 };
+
+void build_kd4(DevRegions& R, cudaStream_t s);
+void build_kd4_mask(const DevRegions& R, const uint8_t* flags, DevBuf<uint8_t>& mask, cudaStream_t s);
 
 void build_active(const DevRegions& R, int kind, int field, double tf_lo, double tf_hi, const double* rgba_host,
                   double iso, DevActive& out, cudaStream_t s);

@@ -18,6 +18,7 @@
 // leaf's brick-id list is already ascending (the reference's np.sort).
 #include "common.cuh"
 #include "scan.cuh"
+#include "accel.cuh"
 #include <algorithm>
 #include <cstdlib>
 
@@ -562,6 +563,7 @@ void build_regions_device(const DevModel& m, DevRegions& out, cudaStream_t s) {
         check_launch("k_metadata");
     }
     XB_CUDA(cudaStreamSynchronize(s));
+    build_kd4(out, s);
     out.has_tree = true;
 }
 

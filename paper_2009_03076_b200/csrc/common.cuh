@@ -135,6 +135,18 @@ struct __align__(8) KdNode {
     int32_t b;  // interior: split plane in half units ; leaf: unused
 };
 
+// Two binary k-d levels collapsed into one 32-byte node (the warp traversal's
+// node, csrc/kd4.cu).  Slots 0..3 are the grandchildren LL, LR, RL, RR (left =
+// below the split plane); when a child of the root split is itself terminal
+// its slot pair holds {child, -1}.  Child codes: >= 0 Kd4 node, -1 empty
+// (cavity / unused), <= -2 leaf region -2 - code.
+struct __align__(16) Kd4Node {
+    int32_t plane[3];  // half units: [0] node split, [1] left child's split, [2] right child's split
+    uint32_t axes;     // bits 0-1 axis of [0]; 2-3 / 4-5 axis of [1] / [2], 3 = child is terminal
+    int32_t child[4];
+};
+static_assert(sizeof(Kd4Node) == 32, "Kd4Node must be 32 bytes");
+
 __host__ __device__ inline uint32_t pack_brick_meta(int level, int nx, int ny, int nz) {
     return (uint32_t)level | ((uint32_t)nx << 5) | ((uint32_t)ny << 14) | ((uint32_t)nz << 23);
 }
@@ -176,6 +188,11 @@ struct DevRegions {
     std::vector<int64_t> kd_level_base;       // BFS level boundaries (L+1 entries)
     int32_t root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};
     DevBuf<KdNode> kd;
+    // the same tree with two levels per node (warp traversal), and the binary
+    // node each slot stands for (to fold active flags into slot masks)
+    int64_t n_kd4 = 0;
+    DevBuf<Kd4Node> kd4;
+    DevBuf<int4> kd4_bin;
     bool has_tree = false;
     // reference-layout arrays for download
     DevBuf<double> lo, hi, finest, vr64;

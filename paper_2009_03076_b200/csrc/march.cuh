@@ -77,8 +77,9 @@ struct SceneView {
     const RegionRec* __restrict__ rec;
     const int32_t* __restrict__ rids;
     const KdNode* __restrict__ kd;
+    const Kd4Node* __restrict__ kd4;
     int32_t root_lo[3], root_hi[3];
-    int64_t n_kd;
+    int64_t n_kd, n_kd4;
 };
 
 // ---------------------------------------------------------------------------
@@ -421,6 +422,135 @@ __device__ __forceinline__ void gather_fast(const SceneView& S, const int32_t* _
     }
 }
 
+// Frame-kernel gather (k_warp): the value sums num/den are the reference's
+// exact FP64 sequence (as gather_fast); the analytic gradient, which only feeds
+// the headlight shading factor (R/render.py:284-289, never alpha, positions
+// or counters), is evaluated in FP32 with the trilinear sums factored per
+// axis.  Per brick, with the hat factors of invalid window cells zeroed,
+//   gnum = sum hx hy hz u,  dn_x = sum sx hy hz u, ...,  dd_x = (sum sx)(sum hy)(sum hz), ...
+// where u = v - v0 (v0 = first contributing cell, R/sampling.py:160-170), so a
+// locally constant field still yields an exactly zero gradient (shade 0.2).
+// g = dn*den - gnum*dd is the reference's quotient-rule numerator; the positive
+// 1/den^2 is dropped because the shading factor depends on the direction only.
+struct FastAccum {
+    double num, den;
+    float g[3];
+    int n_nz;
+};
+
+template <bool GRAD>
+__device__ __forceinline__ void gather_shade(const SceneView& S, const int32_t* __restrict__ ids, int nids, double px,
+                                             double py, double pz, FastAccum& A) {
+    A.num = 0.0;
+    A.den = 0.0;
+    A.n_nz = 0;
+    float fden = 0.f, gnum = 0.f, dn0 = 0.f, dn1 = 0.f, dn2 = 0.f, dd0 = 0.f, dd1 = 0.f, dd2 = 0.f, v0 = 0.f;
+    bool have_ref = false;
+    for (int t = 0; t < nids; t++) {
+        const int b = __ldg(ids + t);
+        const int4 ba = __ldg(S.brick_a + b);
+        const uint32_t bm = __ldg(S.brick_m + b);
+        const int lev = bm & 31;
+        const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
+        const double w = pow2(lev), iw_d = pow2(-lev);
+        const double fx = floor((px - (double)ba.x) * iw_d - 0.5);
+        const double fy = floor((py - (double)ba.y) * iw_d - 0.5);
+        const double fz = floor((pz - (double)ba.z) * iw_d - 0.5);
+        if (!(fx >= -1.0 && fx < (double)nx && fy >= -1.0 && fy < (double)ny && fz >= -1.0 && fz < (double)nz)) continue;
+        const int x0 = (int)fx, y0 = (int)fy, z0 = (int)fz;
+        const double half = 0.5 * w;
+        const double cx0 = (double)(ba.x + x0 * (1 << lev)) + half, cx1 = cx0 + w;
+        const double cy0 = (double)(ba.y + y0 * (1 << lev)) + half, cy1 = cy0 + w;
+        const double cz0 = (double)(ba.z + z0 * (1 << lev)) + half, cz1 = cz0 + w;
+        const double ex0 = cx0 - px, ex1 = cx1 - px, ey0 = cy0 - py, ey1 = cy1 - py, ez0 = cz0 - pz, ez1 = cz1 - pz;
+        double hx0 = 1.0 - fabs(ex0) * iw_d, hx1 = 1.0 - fabs(ex1) * iw_d;
+        double hy0 = 1.0 - fabs(ey0) * iw_d, hy1 = 1.0 - fabs(ey1) * iw_d;
+        double hz0 = 1.0 - fabs(ez0) * iw_d, hz1 = 1.0 - fabs(ez1) * iw_d;
+        // A window cell contributes iff its three axis slots are valid (inside
+        // the brick, hat > 0).  Zeroing the hat of an invalid slot turns every
+        // skipped term into +0 (h) and +-0 (h*v), which leave the running sums
+        // bit-identical, so the 8 cells run branch-free; loads use clamped,
+        // in-brick indices.
+        const bool vx0 = x0 >= 0 && hx0 > 0.0, vx1 = x0 + 1 < nx && hx1 > 0.0;
+        const bool vy0 = y0 >= 0 && hy0 > 0.0, vy1 = y0 + 1 < ny && hy1 > 0.0;
+        const bool vz0 = z0 >= 0 && hz0 > 0.0, vz1 = z0 + 1 < nz && hz1 > 0.0;
+        hx0 = vx0 ? hx0 : 0.0; hx1 = vx1 ? hx1 : 0.0;
+        hy0 = vy0 ? hy0 : 0.0; hy1 = vy1 ? hy1 : 0.0;
+        hz0 = vz0 ? hz0 : 0.0; hz1 = vz1 ? hz1 : 0.0;
+        const int ncx = (int)vx0 + (int)vx1, ncy = (int)vy0 + (int)vy1, ncz = (int)vz0 + (int)vz1;
+        A.n_nz += ncx * ncy * ncz;
+        const int xa = max(x0, 0), xb = min(x0 + 1, nx - 1);
+        const int ya = max(y0, 0), yb = min(y0 + 1, ny - 1);
+        const int za = max(z0, 0), zb = min(z0 + 1, nz - 1);
+        const float* __restrict__ base = S.vals + (uint32_t)ba.w;
+        const int r00 = nx * (ya + ny * za), r01 = nx * (yb + ny * za), r10 = nx * (ya + ny * zb),
+                  r11 = nx * (yb + ny * zb);
+        float vv[2][2][2];  // [dz][dy][dx]
+        vv[0][0][0] = __ldg(base + r00 + xa); vv[0][0][1] = __ldg(base + r00 + xb);
+        vv[0][1][0] = __ldg(base + r01 + xa); vv[0][1][1] = __ldg(base + r01 + xb);
+        vv[1][0][0] = __ldg(base + r10 + xa); vv[1][0][1] = __ldg(base + r10 + xb);
+        vv[1][1][0] = __ldg(base + r11 + xa); vv[1][1][1] = __ldg(base + r11 + xb);
+        const double hxy00 = hx0 * hy0, hxy01 = hx1 * hy0, hxy10 = hx0 * hy1, hxy11 = hx1 * hy1;  // [dy][dx]
+        const double hzz[2] = {hz0, hz1};
+#pragma unroll
+        for (int dz = 0; dz < 2; dz++) {  // z, y, x ascending: the reference's order
+            const double h0 = hxy00 * hzz[dz], h1 = hxy01 * hzz[dz], h2 = hxy10 * hzz[dz], h3 = hxy11 * hzz[dz];
+            A.num += h0 * (double)vv[dz][0][0]; A.den += h0;
+            A.num += h1 * (double)vv[dz][0][1]; A.den += h1;
+            A.num += h2 * (double)vv[dz][1][0]; A.den += h2;
+            A.num += h3 * (double)vv[dz][1][1]; A.den += h3;
+        }
+        if (GRAD) {
+            if (!have_ref && ncx * ncy * ncz > 0) {  // first contributing cell (z, y, x order)
+                v0 = vv[vz0 ? 0 : 1][vy0 ? 0 : 1][vx0 ? 0 : 1];
+                have_ref = true;
+            }
+            const float fw = (float)iw_d;
+            const float ax0 = (float)hx0, ax1 = (float)hx1, ay0 = (float)hy0, ay1 = (float)hy1, az0 = (float)hz0,
+                        az1 = (float)hz1;
+            const float sx0 = vx0 ? (ex0 > 0.0 ? fw : -fw) : 0.f, sx1 = vx1 ? (ex1 > 0.0 ? fw : -fw) : 0.f;
+            const float sy0 = vy0 ? (ey0 > 0.0 ? fw : -fw) : 0.f, sy1 = vy1 ? (ey1 > 0.0 ? fw : -fw) : 0.f;
+            const float sz0 = vz0 ? (ez0 > 0.0 ? fw : -fw) : 0.f, sz1 = vz1 ? (ez1 > 0.0 ? fw : -fw) : 0.f;
+            float C[2], D[2], E[2];
+#pragma unroll
+            for (int dz = 0; dz < 2; dz++) {
+                const float u00 = vv[dz][0][0] - v0, u01 = vv[dz][0][1] - v0;
+                const float u10 = vv[dz][1][0] - v0, u11 = vv[dz][1][1] - v0;
+                const float A0 = fmaf(ax1, u01, ax0 * u00), A1 = fmaf(ax1, u11, ax0 * u10);  // x-hat reductions
+                const float B0 = fmaf(sx1, u01, sx0 * u00), B1 = fmaf(sx1, u11, sx0 * u10);  // x-slope reductions
+                C[dz] = fmaf(ay1, A1, ay0 * A0);  // sum hx hy u
+                D[dz] = fmaf(ay1, B1, ay0 * B0);  // sum sx hy u
+                E[dz] = fmaf(sy1, A1, sy0 * A0);  // sum hx sy u
+            }
+            gnum = fmaf(az1, C[1], fmaf(az0, C[0], gnum));
+            dn0 = fmaf(az1, D[1], fmaf(az0, D[0], dn0));
+            dn1 = fmaf(az1, E[1], fmaf(az0, E[0], dn1));
+            dn2 = fmaf(sz1, C[1], fmaf(sz0, C[0], dn2));
+            const float Hx = ax0 + ax1, Hy = ay0 + ay1, Hz = az0 + az1;
+            const float Sx = sx0 + sx1, Sy = sy0 + sy1, Sz = sz0 + sz1;
+            fden = fmaf(Hx * Hy, Hz, fden);
+            dd0 = fmaf(Sx * Hy, Hz, dd0);
+            dd1 = fmaf(Hx * Sy, Hz, dd1);
+            dd2 = fmaf(Hx * Hy, Sz, dd2);
+        }
+    }
+    if (GRAD) {
+        A.g[0] = dn0 * fden - gnum * dd0;
+        A.g[1] = dn1 * fden - gnum * dd1;
+        A.g[2] = dn2 * fden - gnum * dd2;
+    }
+}
+
+// _shade_factor (R/render.py:284-289) on an unnormalised FP32 gradient direction
+__device__ __forceinline__ double shade_factor_f(const float g[3], const Ray& r) {
+    const float m = fmaxf(fabsf(g[0]), fmaxf(fabsf(g[1]), fabsf(g[2])));
+    if (m == 0.f || !(m < INFINITY)) return 0.2;
+    const float s = 1.f / m;  // scale to [1, 3] before squaring: no under/overflow
+    const float a = g[0] * s, b = g[1] * s, c = g[2] * s;
+    const float dot = a * (float)r.d[0] + b * (float)r.d[1] + c * (float)r.d[2];
+    return 0.2 + 0.8 * (double)(fabsf(dot) * rsqrtf(a * a + b * b + c * c));
+}
+
 __device__ __forceinline__ void analytic_gradient(const Accum& A, double g[3]) {
     // _sample_gradient mode 1, R/render.py:295-306
     if (A.den <= kEpsWeight) { g[0] = g[1] = g[2] = 0.0; return; }
@@ -452,6 +582,33 @@ __device__ __forceinline__ void tf_eval(const double* tf, double tf_lo, double t
 #pragma unroll
     for (int k = 0; k < 4; k++) c[k] = g * tf[i * 4 + k] + f * tf[(i + 1) * 4 + k];
 }
+
+// _tf_eval with the domain reciprocal hoisted: the lerp is continuous across
+// bins, so a last-ulp change of t moves the colour by ~1e-16 only
+__device__ __forceinline__ void tf_eval_fast(const double* tf, double tf_lo, double tf_inv, double v, double c[4]) {
+    double t = (v - tf_lo) * tf_inv;
+    if (t < 0.0) t = 0.0;
+    else if (t > 1.0) t = 1.0;
+    const double x = t * 255.0;
+    const int i = (int)x;
+    if (i >= 255) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) c[k] = tf[255 * 4 + k];
+        return;
+    }
+    const double f = x - (double)i, g = 1.0 - f;
+    const double4 a = *reinterpret_cast<const double4*>(tf + 4 * i);
+    const double4 b = *reinterpret_cast<const double4*>(tf + 4 * i + 4);
+    c[0] = g * a.x + f * b.x;
+    c[1] = g * a.y + f * b.y;
+    c[2] = g * a.z + f * b.z;
+    c[3] = g * a.w + f * b.w;
+}
+
+// opacity correction alpha' = 1 - (1 - a)^y (R/render.py:432) as
+// -expm1(y * log(1 - a)): same rounded base 1 - a as the reference, within a
+// few ulp of pow, and a fraction of pow's code size
+__device__ __forceinline__ double opacity_correct(double a, double y) { return -expm1(y * log(1.0 - a)); }
 
 // central / clamped-central gradient (R/render.py:307-376)
 __device__ inline void central_gradient(const SceneView& S, int mode, double px, double py, double pz, int rid,
@@ -520,6 +677,10 @@ struct MarchConst {
     double iso_value;
     double iso_rgb[3];
     double tf_lo, tf_hi;
+    // host-computed per finest level (IEEE division on the host, same values
+    // as the kernel would compute): dt = fw/(spc*rate), s1 = fw/spc (R/render.py:402-403)
+    double lv_dt[32], lv_s1[32], lv_is1[32];
+    double tf_inv;  // 1/(tf_hi - tf_lo)
 };
 
 struct RayStats {

@@ -327,6 +327,490 @@ __global__ void __launch_bounds__(kFrameThreads, MINB) k_frame(const __grid_cons
 }
 
 // ---------------------------------------------------------------------------
+// k_warp: one warp per ray (default kernel).
+//
+// Traversal is a warp-cooperative *ordered frontier* over the region k-d tree:
+// lane i holds the i-th entry of an ordered list of disjoint subtrees that
+// together cover the rest of the ray (front-to-back order).  One expansion
+// step loads the node of every unresolved entry at once (32 independent loads
+// instead of one dependent chain) and replaces it in place by its children
+// (near child first) or drops it (culled / inactive); resolved leaves keep
+// their place.  The list tail beyond 32 entries spills to a per-warp LIFO in
+// shared memory — every spilled entry lies after everything in the frontier
+// and before everything spilled earlier, so popping restores list order.
+// Culling is the same conservative test as kd_next, so the leaves come out in
+// exactly r_in order.
+//
+// The leading run of leaves is then consumed as a batch: exact slab test per
+// lane, the reference's restart chain t_i = restart(t_out of the previous
+// visited region) (R/render.py:451-453), the lattice count of every segment,
+// a warp prefix sum, and the samples in chunks of 32 — every lane takes one
+// sample of the ray, so the gather runs converged.  Compositing a chunk is a
+// warp scan of the front-to-back "over" operator (T, C) -> (T_a T_b, C_a +
+// T_a C_b); the first lane whose accumulated alpha reaches `early` ends the
+// ray, and the sample / region counters stop exactly there (R/render.py:419,
+// 448-449).  The scan reassociates the alpha recurrence, so alpha differs from
+// the reference by rounding only (~1e-16), like CUDA's pow.
+
+constexpr int kWarpThreads = 128;
+constexpr int kWarpMinBlocks = 4;
+constexpr int kWarpsPerBlock = kWarpThreads / 32;
+constexpr int kWarpStack = 256;  // spilled frontier entries per warp
+constexpr int kRaysPerGrab = 8;  // rays taken per work-counter atomic
+constexpr int kLeafBatch = 32;   // consume once this many leading leaves are resolved
+
+struct SegQ {       // one visited region of the segment queue
+    double ci, co;   // clipped interval
+    double kf;       // first lattice index inside (t_in, t_out)
+    int ids, meta;   // RegionRec.ids_begin / meta
+    int cnt, rid;    // samples, region id
+};
+
+struct SpillEnt {
+    int code;        // >= 0: unresolved k-d node; <= -2: resolved leaf, region -2 - code
+    float tn, tf;    // conservative ray interval of the subtree (rounded outward)
+};
+
+__device__ __forceinline__ double sel3(int a, const double v[3]) { return a == 0 ? v[0] : (a == 1 ? v[1] : v[2]); }
+__device__ __forceinline__ int kd4_child(const Kd4Node& nd, int s) {
+    return s < 2 ? (s == 0 ? nd.child[0] : nd.child[1]) : (s == 2 ? nd.child[2] : nd.child[3]);
+}
+
+// lattice of one region visit (R/render.py:404-418): the samples are the k in
+// [kf, ke) with t_in < dt*(k+rho) < t_out, plus the final one at t_out.
+__device__ __forceinline__ void lattice(double ci, double co, double dt, double rho, double& kf, int& cnt) {
+    double k = floor(ci / dt - rho) + 1.0;
+    for (;;) {  // skipped lattice points (tk <= t_in): at most a couple
+        const double tk = dt * (k + rho);
+        if (tk >= co || tk > ci) break;
+        k += 1.0;
+    }
+    kf = k;
+    double ke = floor(co / dt - rho);
+    if (ke < kf) ke = kf;
+    while (ke > kf && dt * ((ke - 1.0) + rho) >= co) ke -= 1.0;
+    while (dt * (ke + rho) < co) ke += 1.0;
+    cnt = (int)(ke - kf) + 1;
+}
+
+template <int GRAD, bool ISO, bool COUNT, int MINB = kWarpMinBlocks>
+__global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_constant__ RenderArgs A,
+                                                                       int64_t n_slots) {
+    __shared__ double s_tf[1024];
+    __shared__ int s_code[kWarpsPerBlock][32];
+    __shared__ double s_tn[kWarpsPerBlock][32], s_tfar[kWarpsPerBlock][32];
+    __shared__ SpillEnt s_stack[kWarpsPerBlock][kWarpStack];
+    __shared__ SegQ s_q[kWarpsPerBlock][32];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
+    __syncthreads();
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    SpillEnt* __restrict__ stk = s_stack[wid];
+    const SceneView& S = A.S;
+    const double early = A.M.early;
+    unsigned long long tot_reg = 0, tot_smp = 0, tot_bytes = 0;
+
+    for (;;) {
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(A.work_counter, (unsigned long long)kRaysPerGrab);
+        b0 = __shfl_sync(FULL, b0, 0);
+        if ((int64_t)b0 >= n_slots) break;
+        const int64_t b1 = min(n_slots, (int64_t)b0 + kRaysPerGrab);
+        for (int64_t slot = (int64_t)b0; slot < b1; slot++) {
+            const SlotPix sp = slot_pixel(A, slot);
+            if (!sp.live) continue;
+            Ray r;
+            pixel_ray(A, sp.x, sp.y, r);
+            const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
+            double tmin = 0.0, tmax = kTFar;
+            clip_ray(A.M, r, tmin, tmax);
+            double Tr = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;  // transmittance, premultiplied colour
+            int nreg = 0, nsmp = 0;
+            if (tmin < tmax) {
+                if (ISO) tmax = A.iso_tend[slot];
+                double t = tmin;  // the reference's query start (restart chain)
+                // ---- frontier: lane i < n holds list entry i; the rest is on the spill stack
+                int n = 0, spn = 0;
+                int e_code = -1;
+                double e_tn = 0.0, e_tf = 0.0;
+                {
+                    double a, b;
+                    slab_h(S.root_lo, S.root_hi, r, a, b);
+                    if (S.n_kd > 0 && a <= b && A.vflags[0]) {
+                        n = 1;
+                        if (lane == 0) {
+                            // Kd4 node 0 is the binary root when it is interior; a leaf root resolves at once
+                            e_code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
+                            e_tn = a;
+                            e_tf = b;
+                        }
+                    }
+                }
+                bool walk = n > 0;
+                // ---- segment queue: lane i < nq holds visited region i (in ray order)
+                //      and q_P = inclusive prefix of the sample counts; h0 samples of
+                //      the queue are already composited
+                //      (records in the per-warp shared ring s_q from slot qh on)
+                int nq = 0, h0 = 0, tailP = 0, qh = 0;
+                int q_P = 0x7fffffff;
+                SegQ* __restrict__ ring = s_q[wid];
+                for (;;) {
+                    const int pending = tailP - h0;
+                    if (pending >= 32 || (!walk && pending > 0)) {
+                        // ================= one chunk of (up to) 32 samples
+                        const int m = min(32, pending);
+                        const int s = h0 + lane;
+                        const bool act = lane < m;
+                        int sg = 0;  // segment of sample s: #{i : q_P[i] <= s}
+#pragma unroll
+                        for (int b = 16; b >= 1; b >>= 1) {
+                            const int v = __shfl_sync(FULL, q_P, sg + b - 1);
+                            if (v <= s) sg += b;
+                        }
+                        sg = min(sg, 31);
+                        const SegQ sq = ring[(qh + sg) & 31];
+                        const int s_end = __shfl_sync(FULL, q_P, sg);
+                        double Ts = 1.0, Cs0 = 0.0, Cs1 = 0.0, Cs2 = 0.0;
+                        unsigned long long my_bytes = 0;
+                        if (act) {
+                            const int lev = sq.meta >> 24;
+                            const double s_dt = A.M.lv_dt[lev];
+                            const int j = s - (s_end - sq.cnt);
+                            const double prev = j == 0 ? sq.ci : s_dt * ((sq.kf + (double)(j - 1)) + rho);
+                            const double tk = j == sq.cnt - 1 ? sq.co : s_dt * ((sq.kf + (double)j) + rho);
+                            const double sl = tk - prev;
+                            const double mid = 0.5 * (prev + tk);
+                            const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1],
+                                         pz = r.o[2] + mid * r.d[2];
+                            const int nids = sq.meta & 0xffffff;
+                            const int32_t* ids = S.rids + sq.ids;
+                            FastAccum F;
+                            gather_shade<GRAD == 1>(S, ids, nids, px, py, pz, F);
+                            if (COUNT) my_bytes = 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
+                            if (F.den > kEpsWeight) {
+                                const double v = F.num / F.den;
+                                double c[4];
+                                tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_inv, v, c);
+                                if (c[3] > 0.0) {
+                                    const double alpha = opacity_correct(c[3], sl * A.M.lv_is1[lev]);
+                                    if (GRAD != 0) {
+                                        double f;
+                                        if (GRAD == 1) {
+                                            f = shade_factor_f(F.g, r);
+                                        } else {
+                                            double g[3];
+                                            int64_t ne = 0;
+                                            central_gradient(S, A.M.grad_mode, px, py, pz, sq.rid, ids, nids, v, g,
+                                                             &ne);
+                                            f = shade_factor(g, r);
+                                        }
+                                        c[0] *= f; c[1] *= f; c[2] *= f;
+                                    }
+                                    Ts = 1.0 - alpha;
+                                    Cs0 = alpha * c[0];
+                                    Cs1 = alpha * c[1];
+                                    Cs2 = alpha * c[2];
+                                }
+                            }
+                        }
+                        // inclusive scan of the front-to-back "over" operator
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const double pT = __shfl_up_sync(FULL, Ts, o);
+                            const double p0 = __shfl_up_sync(FULL, Cs0, o), p1 = __shfl_up_sync(FULL, Cs1, o),
+                                         p2 = __shfl_up_sync(FULL, Cs2, o);
+                            if (lane >= o) {
+                                Cs0 = p0 + pT * Cs0;
+                                Cs1 = p1 + pT * Cs1;
+                                Cs2 = p2 + pT * Cs2;
+                                Ts = pT * Ts;
+                            }
+                        }
+                        const unsigned tm = __ballot_sync(FULL, act && 1.0 - Tr * Ts >= early);
+                        const int last = tm ? __ffs(tm) - 1 : m - 1;
+                        const double lT = __shfl_sync(FULL, Ts, last);
+                        const double l0 = __shfl_sync(FULL, Cs0, last), l1 = __shfl_sync(FULL, Cs1, last),
+                                     l2 = __shfl_sync(FULL, Cs2, last);
+                        Cr += Tr * l0;
+                        Cg += Tr * l1;
+                        Cb += Tr * l2;
+                        Tr *= lT;
+                        if (COUNT && lane <= last) tot_bytes += my_bytes;
+                        if (tm) {  // early termination (R/render.py:448-449): counters stop here
+                            const int sg_last = __shfl_sync(FULL, sg, last);
+                            nsmp += last + 1;
+                            nreg += sg_last + 1;
+                            if (COUNT && lane <= sg_last)
+                                tot_bytes += 32 + 4 * (unsigned long long)(ring[(qh + lane) & 31].meta & 0xffffff);
+                            break;
+                        }
+                        nsmp += m;
+                        h0 += m;
+                        // drop the fully composited segments from the queue front
+                        const int k = __popc(__ballot_sync(FULL, lane < nq && q_P <= h0));
+                        if (k > 0) {
+                            if (COUNT && lane < k)
+                                tot_bytes += 32 + 4 * (unsigned long long)(ring[(qh + lane) & 31].meta & 0xffffff);
+                            const int done = __shfl_sync(FULL, q_P, k - 1);
+                            q_P = __shfl_down_sync(FULL, q_P, k);
+                            nq -= k;
+                            q_P = lane < nq ? q_P - done : 0x7fffffff;
+                            qh = (qh + k) & 31;
+                            h0 -= done;
+                            tailP -= done;
+                            nreg += k;
+                        }
+                        continue;
+                    }
+                    if (!walk) break;
+                    // ================= traversal
+                    if (n < 32 && spn > 0) {  // refill the frontier from the spill stack (earliest on top)
+                        const int q = min(32 - n, spn);
+                        if (lane >= n && lane < n + q) {
+                            const SpillEnt f = stk[spn - 1 - (lane - n)];
+                            e_code = f.code;
+                            e_tn = (double)f.tn;
+                            e_tf = (double)f.tf;
+                        }
+                        spn -= q;
+                        n += q;
+                        __syncwarp();
+                    }
+                    if (n == 0) {
+                        walk = false;
+                        continue;
+                    }
+                    const unsigned leafm = __ballot_sync(FULL, lane < n && e_code <= -2);
+                    const int nl = leafm == FULL ? 32 : __ffs(~leafm) - 1;
+                    if (nl > 0) {
+                        // ---- consume leading leaves into the segment queue: exact slab,
+                        //      restart chain t_i = restart(t_out of the previous visit)
+                        const int take = min(nl, 32 - nq);  // nq < 32 here: a full queue holds >= 32 samples
+                        const bool isleaf = lane < take;
+                        const int rid = isleaf ? -2 - e_code : 0;
+                        RegionRec rr{};
+                        double r_in = INFINITY, r_out = -INFINITY;
+                        if (isleaf) {
+                            rr = S.rec[rid];
+                            slab_h(rr.lo, rr.hi, r, r_in, r_out);
+                        }
+                        double co = r_out < tmax ? r_out : tmax;
+                        const double prev_co = __shfl_up_sync(FULL, co, 1);
+                        const double ti = lane == 0 ? t : restart_t(prev_co);
+                        double ci = r_in > ti ? r_in : ti;
+                        bool ok = isleaf && ci < co;
+                        const unsigned lmask = take == 32 ? FULL : ((1u << take) - 1u);
+                        unsigned okm = __ballot_sync(FULL, ok);
+                        bool stop = false;
+                        if (okm != lmask) {
+                            // a skipped region (thinner than the restart epsilon, or missed
+                            // by the ray): resolve the chain sequentially
+                            double tt = t;
+                            ok = false;
+                            for (int i = 0; i < take; i++) {
+                                const double ri = __shfl_sync(FULL, r_in, i), ro = __shfl_sync(FULL, r_out, i);
+                                const double a = ri > tt ? ri : tt, b = ro < tmax ? ro : tmax;
+                                if (a < b) {
+                                    if (lane == i) { ok = true; ci = a; co = b; }
+                                    tt = restart_t(b);
+                                    if (tt >= tmax) { stop = true; break; }
+                                }
+                            }
+                            okm = __ballot_sync(FULL, ok);
+                        }
+                        // shift the frontier past the consumed leaves
+                        if (take < 32) {
+                            e_code = __shfl_down_sync(FULL, e_code, take);
+                            e_tn = __shfl_down_sync(FULL, e_tn, take);
+                            e_tf = __shfl_down_sync(FULL, e_tf, take);
+                        }
+                        n -= take;
+                        const int ns = __popc(okm);
+                        if (stop) walk = false;
+                        if (ns == 0) continue;
+                        int g_rid = rid, g_ids = rr.ids_begin, g_meta = rr.meta;
+                        double g_ci = ci, g_co = co;
+                        if (okm != ((ns == 32) ? FULL : ((1u << ns) - 1u))) {
+                            // rare: gather the ns visited lanes via shared scratch
+                            if (ok) {
+                                const int p = __popc(okm & lt_mask);
+                                s_code[wid][p] = rid;
+                                s_tn[wid][p] = ci;
+                                s_tfar[wid][p] = co;
+                            }
+                            __syncwarp();
+                            if (lane < ns) {
+                                g_rid = s_code[wid][lane];
+                                g_ci = s_tn[wid][lane];
+                                g_co = s_tfar[wid][lane];
+                                const RegionRec q = S.rec[g_rid];
+                                g_ids = q.ids_begin;
+                                g_meta = q.meta;
+                            }
+                            __syncwarp();
+                        }
+                        double g_kf = 0.0;
+                        int g_cnt = 0;
+                        if (lane < ns) lattice(g_ci, g_co, A.M.lv_dt[g_meta >> 24], rho, g_kf, g_cnt);
+                        int P = g_cnt;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int v = __shfl_up_sync(FULL, P, o);
+                            if (lane >= o) P += v;
+                        }
+                        const double t_last = __shfl_sync(FULL, g_co, ns - 1);
+                        const int S_new = __shfl_sync(FULL, P, 31);
+                        // append: new segment i -> window position nq + i
+                        if (lane < ns) {
+                            SegQ& q = ring[(qh + nq + lane) & 31];
+                            q.ci = g_ci; q.co = g_co; q.kf = g_kf;
+                            q.ids = g_ids; q.meta = g_meta; q.cnt = g_cnt; q.rid = g_rid;
+                        }
+                        const int u_P = __shfl_up_sync(FULL, P, nq);
+                        if (lane >= nq && lane < nq + ns) q_P = tailP + u_P;
+                        __syncwarp();
+                        nq += ns;
+                        tailP += S_new;
+                        t = restart_t(t_last);
+                        if (t >= tmax) walk = false;
+                        continue;
+                    }
+                    // ---- expansion step: every unresolved entry is a Kd4 node; it is
+                    //      replaced in place by its (up to 4) surviving children, near first
+                    bool actx = lane < n && e_code >= 0;
+                    if (spn + 96 > kWarpStack) {  // near the spill limit: expand the first entry only
+                        const unsigned um = __ballot_sync(FULL, actx);
+                        actx = actx && lane == __ffs(um) - 1;
+                    }
+                    int oc[4] = {0, 0, 0, 0};
+                    double otn[4] = {0.0, 0.0, 0.0, 0.0}, otf[4] = {0.0, 0.0, 0.0, 0.0};
+                    bool ov[4] = {false, false, false, false};  // candidate k: half k/2, child k%2
+                    if (actx) {
+                        const Kd4Node nd = S.kd4[e_code];
+                        const uint32_t msk = A.vmask4[e_code];
+                        int hs[2] = {0, 0};
+                        double hn[2] = {0.0, 0.0}, hf[2] = {0.0, 0.0};
+                        int nh = 0;
+                        {
+                            const int ax = nd.axes & 3;
+                            const double p = (double)nd.plane[0] * 0.5;
+                            const double da = sel3(ax, r.d), oa = sel3(ax, r.o);
+                            if (da == 0.0) {
+                                hs[0] = oa < p ? 0 : 1; hn[0] = e_tn; hf[0] = e_tf; nh = 1;
+                            } else {
+                                const double tp = (p - oa) * sel3(ax, r.inv);
+                                const int ns_ = da > 0.0 ? 0 : 1;
+                                if (tp >= e_tf) {
+                                    hs[0] = ns_; hn[0] = e_tn; hf[0] = e_tf; nh = 1;
+                                } else if (tp <= e_tn) {
+                                    hs[0] = 1 - ns_; hn[0] = e_tn; hf[0] = e_tf; nh = 1;
+                                } else {
+                                    hs[0] = ns_; hn[0] = e_tn; hf[0] = tp;
+                                    hs[1] = 1 - ns_; hn[1] = tp; hf[1] = e_tf;
+                                    nh = 2;
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            if (h < nh) {
+                                const int sd = hs[h];
+                                const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
+                                int s0 = 2 * sd, s1 = -1;
+                                double a0 = hn[h], bb0 = hf[h], a1 = 0.0, bb1 = 0.0;
+                                if (ax != 3) {
+                                    const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
+                                    const double da = sel3(ax, r.d), oa = sel3(ax, r.o);
+                                    if (da == 0.0) {
+                                        s0 = 2 * sd + (oa < p ? 0 : 1);
+                                    } else {
+                                        const double tp = (p - oa) * sel3(ax, r.inv);
+                                        const int nqq = da > 0.0 ? 0 : 1;
+                                        if (tp >= bb0) {
+                                            s0 = 2 * sd + nqq;
+                                        } else if (tp <= a0) {
+                                            s0 = 2 * sd + 1 - nqq;
+                                        } else {
+                                            s0 = 2 * sd + nqq; bb0 = tp;
+                                            s1 = 2 * sd + 1 - nqq; a1 = tp; bb1 = hf[h];
+                                        }
+                                    }
+                                }
+                                // cull: inactive subtree, or entirely before t / after tmax
+                                ov[2 * h] = ((msk >> s0) & 1) && bb0 > t && a0 < tmax;
+                                oc[2 * h] = kd4_child(nd, s0); otn[2 * h] = a0; otf[2 * h] = bb0;
+                                ov[2 * h + 1] = s1 >= 0 && ((msk >> s1) & 1) && bb1 > t && a1 < tmax;
+                                oc[2 * h + 1] = kd4_child(nd, s1 < 0 ? 0 : s1); otn[2 * h + 1] = a1; otf[2 * h + 1] = bb1;
+                            }
+                        }
+                    } else if (lane < n) {
+                        ov[0] = true;  // resolved leaf (behind the front): stays in place
+                        oc[0] = e_code; otn[0] = e_tn; otf[0] = e_tf;
+                    }
+                    const int cnt = (int)ov[0] + (int)ov[1] + (int)ov[2] + (int)ov[3];
+                    const unsigned m1 = __ballot_sync(FULL, cnt & 1), m2 = __ballot_sync(FULL, cnt & 2),
+                                   m4 = __ballot_sync(FULL, cnt & 4);
+                    const int pos = __popc(m1 & lt_mask) + 2 * __popc(m2 & lt_mask) + 4 * __popc(m4 & lt_mask);
+                    const int total = __popc(m1) + 2 * __popc(m2) + 4 * __popc(m4);
+                    if (spn + max(0, total - 32) > kWarpStack) __trap();  // cannot happen: see the guard above
+                    int p = pos;
+#pragma unroll
+                    for (int c = 0; c < 4; c++) {
+                        if (ov[c]) {
+                            if (p < 32) {
+                                s_code[wid][p] = oc[c];
+                                s_tn[wid][p] = otn[c];
+                                s_tfar[wid][p] = otf[c];
+                            } else {
+                                SpillEnt& f = stk[spn + (total - 1 - p)];
+                                f.code = oc[c];
+                                f.tn = __double2float_rd(otn[c]);
+                                f.tf = __double2float_ru(otf[c]);
+                            }
+                            p++;
+                        }
+                    }
+                    __syncwarp();
+                    if (total > 32) spn += total - 32;
+                    n = min(total, 32);
+                    if (lane < n) {
+                        e_code = s_code[wid][lane];
+                        e_tn = s_tn[wid][lane];
+                        e_tf = s_tfar[wid][lane];
+                    }
+                    __syncwarp();
+                }
+            }
+            if (lane == 0) {
+                double acc[4] = {Cr, Cg, Cb, 1.0 - Tr};
+                if (ISO && tmin < tmax) {
+                    const double f = A.iso_shade[slot];
+                    if (f >= 0.0) {
+                        const double wgt = 1.0 - acc[3];
+                        acc[0] += wgt * A.M.iso_rgb[0] * f;
+                        acc[1] += wgt * A.M.iso_rgb[1] * f;
+                        acc[2] += wgt * A.M.iso_rgb[2] * f;
+                        acc[3] = 1.0;
+                    }
+                }
+                write_pixel(A, sp.out, acc, nreg, nsmp);
+                tot_reg += nreg;
+                tot_smp += nsmp;
+            }
+        }
+    }
+    if (COUNT) {
+        for (int o = 16; o > 0; o >>= 1) tot_bytes += __shfl_xor_sync(FULL, tot_bytes, o);
+    }
+    if (lane == 0 && A.stats) {
+        atomicAdd(&A.stats[0], tot_reg);
+        atomicAdd(&A.stats[1], tot_smp);
+        if (COUNT) atomicAdd(&A.stats[2], tot_bytes);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // simple tile kernel (one thread per pixel), kept for A/B comparison
 
 template <int GRAD, bool ISO, bool COUNT>
@@ -396,9 +880,17 @@ static RenderFn tile_fn(bool count) {
 
 static int grad_index(int mode) { return mode == 0 ? 0 : (mode == 1 ? 1 : 2); }
 
-static bool use_tile_kernel() {
+template <int GRAD, bool ISO>
+static FrameFn warp_fn(bool count) {
+    return count ? (FrameFn)k_warp<GRAD, ISO, true> : (FrameFn)k_warp<GRAD, ISO, false>;
+}
+
+// XB_KERNEL=frame | tile selects the per-lane kernels for A/B measurements
+static int kernel_choice() {
     const char* e = getenv("XB_KERNEL");
-    return e && strcmp(e, "tile") == 0;
+    if (e && strcmp(e, "tile") == 0) return 2;
+    if (e && strcmp(e, "frame") == 0) return 1;
+    return 0;
 }
 
 void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaStream_t s) {
@@ -411,7 +903,8 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         const void* fn = count ? (const void*)k_iso_pass<true> : (const void*)k_iso_pass<false>;
         XB_CUDA(cudaLaunchKernel(fn, dim3(grid_for(n_slots, 128)), dim3(128), args, 0, s));
     }
-    if (use_tile_kernel()) {
+    const int kc = kernel_choice();
+    if (kc == 2) {
         RenderFn fn;
         if (g == 0) fn = iso ? tile_fn<0, true>(count) : tile_fn<0, false>(count);
         else if (g == 1) fn = iso ? tile_fn<1, true>(count) : tile_fn<1, false>(count);
@@ -421,22 +914,38 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         return;
     }
     FrameFn fn;
-    if (g == 0) fn = iso ? frame_fn<0, true>(count) : frame_fn<0, false>(count);
-    else if (g == 1) fn = iso ? frame_fn<1, true>(count) : frame_fn<1, false>(count);
-    else fn = iso ? frame_fn<2, true>(count) : frame_fn<2, false>(count);
-    if (g == 1 && !iso && !count && (getenv("XB_KSTEPS") || getenv("XB_MINB"))) {
-        const int ks = getenv("XB_KSTEPS") ? atoi(getenv("XB_KSTEPS")) : kKdSteps;
-        const int mb = getenv("XB_MINB") ? atoi(getenv("XB_MINB")) : 4;
-        if (FrameFn t = tuned_fn(ks, mb)) fn = t;
+    int threads;
+    if (kc == 1) {
+        threads = kFrameThreads;
+        if (g == 0) fn = iso ? frame_fn<0, true>(count) : frame_fn<0, false>(count);
+        else if (g == 1) fn = iso ? frame_fn<1, true>(count) : frame_fn<1, false>(count);
+        else fn = iso ? frame_fn<2, true>(count) : frame_fn<2, false>(count);
+        if (g == 1 && !iso && !count && (getenv("XB_KSTEPS") || getenv("XB_MINB"))) {
+            const int ks = getenv("XB_KSTEPS") ? atoi(getenv("XB_KSTEPS")) : kKdSteps;
+            const int mb = getenv("XB_MINB") ? atoi(getenv("XB_MINB")) : 4;
+            if (FrameFn t = tuned_fn(ks, mb)) fn = t;
+        }
+    } else {
+        threads = kWarpThreads;
+        if (g == 0) fn = iso ? warp_fn<0, true>(count) : warp_fn<0, false>(count);
+        else if (g == 1) fn = iso ? warp_fn<1, true>(count) : warp_fn<1, false>(count);
+        else fn = iso ? warp_fn<2, true>(count) : warp_fn<2, false>(count);
+        if (g == 1 && !iso && !count && getenv("XB_WMINB")) {  // occupancy sweep (tools/ab.py)
+            const int mb = atoi(getenv("XB_WMINB"));
+            if (mb == 2) fn = (FrameFn)k_warp<1, false, false, 2>;
+            if (mb == 3) fn = (FrameFn)k_warp<1, false, false, 3>;
+            if (mb == 5) fn = (FrameFn)k_warp<1, false, false, 5>;
+        }
     }
     int dev = 0, sms = 0, per_sm = 0;
     XB_CUDA(cudaGetDevice(&dev));
     XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kFrameThreads, 0));
-    const int64_t want = (n_slots + kFrameThreads - 1) / kFrameThreads;
+    XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0));
+    const int64_t per_thread = kc == 1 ? 1 : 32;  // k_warp: one ray per warp at a time
+    const int64_t want = (n_slots * per_thread + threads - 1) / threads;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), want));
     void* args[] = {(void*)&A, (void*)&n_slots};
-    XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(kFrameThreads), args, 0, s));
+    XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(threads), args, 0, s));
 }
 
 // ---------------------------------------------------------------------------

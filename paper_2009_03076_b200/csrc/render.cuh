@@ -14,6 +14,7 @@ constexpr int kFrameMinBlocks = 4;      // 128 regs/thread -> 16 warps/SM (more 
 struct RenderArgs {
     SceneView S;
     const uint8_t* vflags;  // per k-d node: subtree holds an active volume region
+    const uint8_t* vmask4;  // per Kd4 node: active bit per child slot (k_warp)
     const uint8_t* iflags;  // same for the iso predicate
     MarchConst M;
     int W, H;

@@ -97,11 +97,11 @@ class TiledRenderer:
 
         stream = self.torch.cuda.current_stream().cuda_stream
         if self.world == 1:
-            render_native(self.scene, camera, tf, params, self.image.data_ptr(), stream=stream)
+            render_native(self.scene, camera, tf, params, self.image.data_ptr(), stream=stream, sync=False)
             return self.image
         if self.n_local:
             render_native(self.scene, camera, tf, params, self.packed.data_ptr(), tile_rank=self.rank,
-                          tile_world=self.world, stream=stream)
+                          tile_world=self.world, stream=stream, sync=False)
         if not gather:
             return None
         self.dist.all_gather_into_tensor(self.gathered, self.packed)

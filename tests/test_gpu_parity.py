@@ -200,8 +200,23 @@ def _params(meta):
                        seed=meta["seed"], gradient_mode=meta["gradient_mode"], clip_planes=planes)
 
 
+@pytest.fixture
+def kernel_env(request):
+    """XB_KERNEL selects the march kernel: warp (default), frame (per-lane persistent), tile."""
+    import os
+
+    old = os.environ.pop("XB_KERNEL", None)
+    if request.param != "warp":
+        os.environ["XB_KERNEL"] = request.param
+    yield request.param
+    os.environ.pop("XB_KERNEL", None)
+    if old is not None:
+        os.environ["XB_KERNEL"] = old
+
+
+@pytest.mark.parametrize("kernel_env", ["warp", "frame", "tile"], indirect=True)
 @pytest.mark.parametrize("key", _frame_keys())
-def test_frames_match_reference(xb, key, frames):
+def test_frames_match_reference(xb, key, frames, kernel_env):
     from paper_2009_03076_b200.accel import TransferFunction
     from paper_2009_03076_b200.render import build_scene, render_frame, render_frame_float
 
@@ -354,17 +369,19 @@ def test_acceptance_million_cells_vs_oracle(xb):
     assert np.abs(f64.reshape(-1, 4)[rows] - of).max() <= RGBA_TOL
     assert np.array_equal(cnt.reshape(-1, 2)[rows, 0], pr)
     assert np.array_equal(cnt.reshape(-1, 2)[rows, 1], ps)
-    # whole frame: the persistent kernel (dynamic per-lane ray refill) must equal
-    # the one-thread-per-pixel kernel everywhere, on every repetition
+    # whole frame: the warp-per-ray kernel (default) must equal the per-lane
+    # persistent kernel and the one-thread-per-pixel kernel everywhere, on every
+    # repetition
     import os
 
-    os.environ["XB_KERNEL"] = "tile"
-    try:
-        u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)
-    finally:
-        del os.environ["XB_KERNEL"]
-    assert np.array_equal(cnt, cntt)
-    assert np.abs(f64 - f64t).max() <= RGBA_TOL
+    for kern in ("tile", "frame"):
+        os.environ["XB_KERNEL"] = kern
+        try:
+            u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)
+        finally:
+            del os.environ["XB_KERNEL"]
+        assert np.array_equal(cnt, cntt), kern
+        assert np.abs(f64 - f64t).max() <= RGBA_TOL, kern
     for _ in range(3):
         u8r, f64r, cntr, str_ = render_frame_float(scene, cam, tf, params)
         assert np.array_equal(cntr, cnt) and np.array_equal(u8r, u8)

@@ -1,0 +1,64 @@
+"""A/B frame timing of march-kernel variants (XB_KERNEL values), interleaved:
+python tools/ab.py CONFIG warp,frame [reps]"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2009_03076_b200.bricks import build_bricks  # noqa: E402
+from paper_2009_03076_b200.regions import build_regions  # noqa: E402
+from paper_2009_03076_b200.render import MarchParams, build_scene, render_native  # noqa: E402
+
+cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
+variants = (sys.argv[2] if len(sys.argv) > 2 else "warp,frame").split(",")
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+cells = bench.make_cells(cfg)
+model, _ = build_bricks(cells)
+regions = build_regions(model)
+tf = bench.tf_for(model.value_range(0), cfg)
+scene = build_scene(model, regions, tf)
+cam = bench.camera_for(regions.bounds, cfg, 0)
+params = MarchParams(seed=0, gradient_mode=cfg["gradient"])
+W, H = cfg["res"]
+out = torch.empty((H, W, 4), dtype=torch.uint8, device="cuda")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+stream = torch.cuda.current_stream()
+
+
+def setv(v):
+    """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N)"""
+    os.environ.pop("XB_KERNEL", None)
+    os.environ.pop("XB_WMINB", None)
+    if v.startswith("warp") and len(v) > 4:
+        os.environ["XB_WMINB"] = v[4:]
+    elif v != "warp":
+        os.environ["XB_KERNEL"] = v
+
+
+times = {v: [] for v in variants}
+for v in variants:
+    setv(v)
+    for _ in range(3):
+        render_native(scene, cam, tf, params, out.data_ptr(), stream=stream.cuda_stream)
+torch.cuda.synchronize()
+# enqueue everything first (no host sync inside the loop): the GPU queue stays
+# ahead of the host, so host-side stalls never land between two events
+evs = []
+for it in range(reps):
+    for v in variants:
+        setv(v)
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        render_native(scene, cam, tf, params, out.data_ptr(), stream=stream.cuda_stream, sync=False)
+        b.record(stream)
+        evs.append((v, a, b))
+torch.cuda.synchronize()
+for v, a, b in evs:
+    times[v].append(a.elapsed_time(b))
+for v in variants:
+    t = np.array(times[v])
+    print(f"{v:8s} median {np.median(t):8.3f} ms  min {t.min():8.3f}  max {t.max():8.3f}  all {np.round(t, 2).tolist()}")

@@ -30,10 +30,11 @@ res = {}
 for v in variants:
     for k in ("XB_KERNEL", "XB_KSTEPS", "XB_MINB"):
         os.environ.pop(k, None)
-    if v == "tile":
-        os.environ["XB_KERNEL"] = "tile"
+    if v in ("tile", "frame"):
+        os.environ["XB_KERNEL"] = v
     elif v != "default":
         ks, mb = v.split("x")
+        os.environ["XB_KERNEL"] = "frame"
         os.environ["XB_KSTEPS"], os.environ["XB_MINB"] = ks, mb
     for _ in range(3):
         render_native(scene, cam, tf, params, out.data_ptr(), stream=stream.cuda_stream)
