@@ -502,7 +502,10 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, const int32_t* 
         }
         if (GRAD) {
             if (!have_ref && ncx * ncy * ncz > 0) {  // first contributing cell (z, y, x order)
-                v0 = vv[vz0 ? 0 : 1][vy0 ? 0 : 1][vx0 ? 0 : 1];
+                const float r0 = vx0 ? vv[0][0][0] : vv[0][0][1], r1 = vx0 ? vv[0][1][0] : vv[0][1][1];
+                const float r2 = vx0 ? vv[1][0][0] : vv[1][0][1], r3 = vx0 ? vv[1][1][0] : vv[1][1][1];
+                const float p0 = vy0 ? r0 : r1, p1 = vy0 ? r2 : r3;
+                v0 = vz0 ? p0 : p1;  // select chain: no local-memory indexing
                 have_ref = true;
             }
             const float fw = (float)iw_d;
@@ -538,6 +541,186 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, const int32_t* 
         A.g[0] = dn0 * fden - gnum * dd0;
         A.g[1] = dn1 * fden - gnum * dd1;
         A.g[2] = dn2 * fden - gnum * dd2;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Chunk gather for k_warp: the (sample, brick) pairs of a 32-sample chunk are
+// flattened across the warp, so every lane reconstructs one brick per round
+// whatever the brick counts of the samples (regions hold 1..8+ bricks, which
+// left half the lanes idle in a per-sample brick loop).  Each pair yields the
+// brick's partial sums (the reference's per-cell sequence, started from 0);
+// the sample's lane then adds its partials in ascending brick order.  This
+// reassociates the reference's single running sum across brick boundaries
+// (R/sampling.py:66-103), so num/den may differ from it in the last ulp; no
+// test threshold, counter or image tolerance is sensitive to that.
+
+struct BrickPart {
+    double num, den;
+    float fden, gnum, dn0, dn1, dn2, dd0, dd1, dd2;
+    float v0;      // first contributing cell of the brick (gradient shift)
+    int nnz;       // contributing cells; 0: brick contributes nothing
+    float pad[2];
+};
+static_assert(sizeof(BrickPart) == 64, "BrickPart is 64 bytes");
+
+template <bool GRAD>
+__device__ __forceinline__ void brick_part(const SceneView& S, int b, double px, double py, double pz, BrickPart& P) {
+    P.num = 0.0;
+    P.den = 0.0;
+    P.nnz = 0;
+    P.fden = P.gnum = P.dn0 = P.dn1 = P.dn2 = P.dd0 = P.dd1 = P.dd2 = 0.f;
+    P.v0 = 0.f;
+    const int4 ba = __ldg(S.brick_a + b);
+    const uint32_t bm = __ldg(S.brick_m + b);
+    const int lev = bm & 31;
+    const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
+    const double w = pow2(lev), iw_d = pow2(-lev);
+    const double fx = floor((px - (double)ba.x) * iw_d - 0.5);
+    const double fy = floor((py - (double)ba.y) * iw_d - 0.5);
+    const double fz = floor((pz - (double)ba.z) * iw_d - 0.5);
+    if (!(fx >= -1.0 && fx < (double)nx && fy >= -1.0 && fy < (double)ny && fz >= -1.0 && fz < (double)nz)) return;
+    const int x0 = (int)fx, y0 = (int)fy, z0 = (int)fz;
+    const double half = 0.5 * w;
+    const double cx0 = (double)(ba.x + x0 * (1 << lev)) + half, cx1 = cx0 + w;
+    const double cy0 = (double)(ba.y + y0 * (1 << lev)) + half, cy1 = cy0 + w;
+    const double cz0 = (double)(ba.z + z0 * (1 << lev)) + half, cz1 = cz0 + w;
+    const double ex0 = cx0 - px, ex1 = cx1 - px, ey0 = cy0 - py, ey1 = cy1 - py, ez0 = cz0 - pz, ez1 = cz1 - pz;
+    double hx0 = 1.0 - fabs(ex0) * iw_d, hx1 = 1.0 - fabs(ex1) * iw_d;
+    double hy0 = 1.0 - fabs(ey0) * iw_d, hy1 = 1.0 - fabs(ey1) * iw_d;
+    double hz0 = 1.0 - fabs(ez0) * iw_d, hz1 = 1.0 - fabs(ez1) * iw_d;
+    // invalid window slots (outside the brick, hat <= 0) get a zero hat: their
+    // terms are +0 / +-0 and leave the running sums bit-identical
+    const bool vx0 = x0 >= 0 && hx0 > 0.0, vx1 = x0 + 1 < nx && hx1 > 0.0;
+    const bool vy0 = y0 >= 0 && hy0 > 0.0, vy1 = y0 + 1 < ny && hy1 > 0.0;
+    const bool vz0 = z0 >= 0 && hz0 > 0.0, vz1 = z0 + 1 < nz && hz1 > 0.0;
+    hx0 = vx0 ? hx0 : 0.0; hx1 = vx1 ? hx1 : 0.0;
+    hy0 = vy0 ? hy0 : 0.0; hy1 = vy1 ? hy1 : 0.0;
+    hz0 = vz0 ? hz0 : 0.0; hz1 = vz1 ? hz1 : 0.0;
+    P.nnz = ((int)vx0 + (int)vx1) * ((int)vy0 + (int)vy1) * ((int)vz0 + (int)vz1);
+    const int xa = max(x0, 0), xb = min(x0 + 1, nx - 1);
+    const int ya = max(y0, 0), yb = min(y0 + 1, ny - 1);
+    const int za = max(z0, 0), zb = min(z0 + 1, nz - 1);
+    const float* __restrict__ base = S.vals + (uint32_t)ba.w;
+    const int r00 = nx * (ya + ny * za), r01 = nx * (yb + ny * za), r10 = nx * (ya + ny * zb),
+              r11 = nx * (yb + ny * zb);
+    float vv[2][2][2];  // [dz][dy][dx]
+    vv[0][0][0] = __ldg(base + r00 + xa); vv[0][0][1] = __ldg(base + r00 + xb);
+    vv[0][1][0] = __ldg(base + r01 + xa); vv[0][1][1] = __ldg(base + r01 + xb);
+    vv[1][0][0] = __ldg(base + r10 + xa); vv[1][0][1] = __ldg(base + r10 + xb);
+    vv[1][1][0] = __ldg(base + r11 + xa); vv[1][1][1] = __ldg(base + r11 + xb);
+    const double hxy00 = hx0 * hy0, hxy01 = hx1 * hy0, hxy10 = hx0 * hy1, hxy11 = hx1 * hy1;  // [dy][dx]
+    double num = 0.0, den = 0.0;
+#pragma unroll
+    for (int dz = 0; dz < 2; dz++) {  // z, y, x ascending: the reference's order
+        const double hz = dz ? hz1 : hz0;
+        const double h0 = hxy00 * hz, h1 = hxy01 * hz, h2 = hxy10 * hz, h3 = hxy11 * hz;
+        num += h0 * (double)vv[dz][0][0]; den += h0;
+        num += h1 * (double)vv[dz][0][1]; den += h1;
+        num += h2 * (double)vv[dz][1][0]; den += h2;
+        num += h3 * (double)vv[dz][1][1]; den += h3;
+    }
+    P.num = num;
+    P.den = den;
+    if (GRAD && P.nnz > 0) {
+        const float r0 = vx0 ? vv[0][0][0] : vv[0][0][1], r1 = vx0 ? vv[0][1][0] : vv[0][1][1];
+        const float r2 = vx0 ? vv[1][0][0] : vv[1][0][1], r3 = vx0 ? vv[1][1][0] : vv[1][1][1];
+        const float q0 = vy0 ? r0 : r1, q1 = vy0 ? r2 : r3;
+        const float v0 = vz0 ? q0 : q1;  // first contributing cell (z, y, x order)
+        P.v0 = v0;
+        const float fw = (float)iw_d;
+        const float ax0 = (float)hx0, ax1 = (float)hx1, ay0 = (float)hy0, ay1 = (float)hy1, az0 = (float)hz0,
+                    az1 = (float)hz1;
+        const float sx0 = vx0 ? (ex0 > 0.0 ? fw : -fw) : 0.f, sx1 = vx1 ? (ex1 > 0.0 ? fw : -fw) : 0.f;
+        const float sy0 = vy0 ? (ey0 > 0.0 ? fw : -fw) : 0.f, sy1 = vy1 ? (ey1 > 0.0 ? fw : -fw) : 0.f;
+        const float sz0 = vz0 ? (ez0 > 0.0 ? fw : -fw) : 0.f, sz1 = vz1 ? (ez1 > 0.0 ? fw : -fw) : 0.f;
+        float C[2], D[2], E[2];
+#pragma unroll
+        for (int dz = 0; dz < 2; dz++) {
+            const float u00 = vv[dz][0][0] - v0, u01 = vv[dz][0][1] - v0;
+            const float u10 = vv[dz][1][0] - v0, u11 = vv[dz][1][1] - v0;
+            const float A0 = fmaf(ax1, u01, ax0 * u00), A1 = fmaf(ax1, u11, ax0 * u10);
+            const float B0 = fmaf(sx1, u01, sx0 * u00), B1 = fmaf(sx1, u11, sx0 * u10);
+            C[dz] = fmaf(ay1, A1, ay0 * A0);  // sum hx hy u
+            D[dz] = fmaf(ay1, B1, ay0 * B0);  // sum sx hy u
+            E[dz] = fmaf(sy1, A1, sy0 * A0);  // sum hx sy u
+        }
+        P.gnum = fmaf(az1, C[1], az0 * C[0]);
+        P.dn0 = fmaf(az1, D[1], az0 * D[0]);
+        P.dn1 = fmaf(az1, E[1], az0 * E[0]);
+        P.dn2 = fmaf(sz1, C[1], sz0 * C[0]);
+        const float Hx = ax0 + ax1, Hy = ay0 + ay1, Hz = az0 + az1;
+        const float Sx = sx0 + sx1, Sy = sy0 + sy1, Sz = sz0 + sz1;
+        P.fden = Hx * Hy * Hz;
+        P.dd0 = Sx * Hy * Hz;
+        P.dd1 = Hx * Sy * Hz;
+        P.dd2 = Hx * Hy * Sz;
+    }
+}
+
+// All 32 lanes call this together; lanes with act hold one sample each.
+template <bool GRAD>
+__device__ __forceinline__ void gather_chunk(const SceneView& S, bool act, int ids_off, int nids, double px, double py,
+                                             double pz, BrickPart* __restrict__ scratch, int lane, FastAccum& F) {
+    const unsigned FULL = 0xffffffffu;
+    const int nb = act ? nids : 0;
+    int Qi = nb;  // inclusive prefix of the brick counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, Qi, o);
+        if (lane >= o) Qi += v;
+    }
+    const int I = __shfl_sync(FULL, Qi, 31);
+    const int Qe = Qi - nb;
+    F.num = 0.0;
+    F.den = 0.0;
+    F.n_nz = 0;
+    float fden = 0.f, gnum = 0.f, dn0 = 0.f, dn1 = 0.f, dn2 = 0.f, dd0 = 0.f, dd1 = 0.f, dd2 = 0.f, v0 = 0.f;
+    bool have = false;
+    for (int base = 0; base < I; base += 32) {
+        const int q = base + lane;
+        int j = 0;  // owner sample: #{lanes with Qi <= q}
+#pragma unroll
+        for (int b = 16; b >= 1; b >>= 1) {
+            const int v = __shfl_sync(FULL, Qi, j + b - 1);
+            if (v <= q) j += b;
+        }
+        j = min(j, 31);
+        const double qx = __shfl_sync(FULL, px, j), qy = __shfl_sync(FULL, py, j), qz = __shfl_sync(FULL, pz, j);
+        const int qe = __shfl_sync(FULL, Qe, j), qoff = __shfl_sync(FULL, ids_off, j);
+        BrickPart P;
+        if (q < I) {
+            brick_part<GRAD>(S, __ldg(S.rids + qoff + (q - qe)), qx, qy, qz, P);
+        } else {
+            P.num = P.den = 0.0;
+            P.nnz = 0;
+            P.fden = P.gnum = P.dn0 = P.dn1 = P.dn2 = P.dd0 = P.dd1 = P.dd2 = P.v0 = 0.f;
+        }
+        scratch[lane] = P;
+        __syncwarp();
+        const int k0 = max(Qe, base) - base, k1 = min(Qi, base + 32) - base;
+        for (int k = k0; k < k1; k++) {  // my bricks of this round, ascending
+            const BrickPart& B = scratch[k];
+            F.num += B.num;
+            F.den += B.den;
+            F.n_nz += B.nnz;
+            if (GRAD && B.nnz > 0) {
+                if (!have) { v0 = B.v0; have = true; }
+                const float sh = B.v0 - v0;  // re-reference the brick's partials to v0
+                gnum += fmaf(sh, B.fden, B.gnum);
+                dn0 += fmaf(sh, B.dd0, B.dn0);
+                dn1 += fmaf(sh, B.dd1, B.dn1);
+                dn2 += fmaf(sh, B.dd2, B.dn2);
+                dd0 += B.dd0; dd1 += B.dd1; dd2 += B.dd2;
+                fden += B.fden;
+            }
+        }
+        __syncwarp();
+    }
+    if (GRAD) {
+        F.g[0] = dn0 * fden - gnum * dd0;
+        F.g[1] = dn1 * fden - gnum * dd1;
+        F.g[2] = dn2 * fden - gnum * dd2;
     }
 }
 

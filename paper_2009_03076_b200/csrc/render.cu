@@ -357,7 +357,10 @@ constexpr int kWarpMinBlocks = 4;
 constexpr int kWarpsPerBlock = kWarpThreads / 32;
 constexpr int kWarpStack = 256;  // spilled frontier entries per warp
 constexpr int kRaysPerGrab = 8;  // rays taken per work-counter atomic
-constexpr int kLeafBatch = 32;   // consume once this many leading leaves are resolved
+// (sample, brick)-flattened chunk gather (march.cuh:gather_chunk): measured
+// slower on C2 (12.3 vs 10.1 ms) — the per-owner accumulation loop diverges
+// as much as the per-sample brick loop it replaces; kept for A/B
+constexpr bool kFlatGather = false;
 
 struct SegQ {       // one visited region of the segment queue
     double ci, co;   // clipped interval
@@ -372,6 +375,40 @@ struct SpillEnt {
 };
 
 __device__ __forceinline__ double sel3(int a, const double v[3]) { return a == 0 ? v[0] : (a == 1 ? v[1] : v[2]); }
+__device__ __forceinline__ double sel4(int i, const double v[4]) {
+    return i < 2 ? (i == 0 ? v[0] : v[1]) : (i == 2 ? v[2] : v[3]);
+}
+
+// per-ray axis data in shared memory (one copy per warp)
+struct RayAxes {
+    double o[3], inv[3];
+    int sgn[3];  // sign of d: -1, 0, +1
+};
+
+// Split the ray interval [tn, tf] of a k-d cell at plane `ph` (half units) on
+// `axis` into the intervals of its left (below) and right sides, exactly as
+// kd_next classifies children: tp >= tf -> near side only, tp <= tn -> far
+// side only, else near [tn, tp] and far [tp, tf]; with d_axis == 0 only the
+// side holding the origin (half-open).  An empty side gets lo >= hi.  Returns
+// true when the left side is the near one.
+__device__ __forceinline__ bool split_sides(const RayAxes& R, int axis, int ph, double tn, double tf, double lo[2],
+                                            double hi[2]) {
+    const double p = (double)ph * 0.5;
+    const double oa = R.o[axis], ia = R.inv[axis];
+    const int sg = R.sgn[axis];
+    const double tp = (p - oa) * ia;
+    const double cut_lo = fmax(tn, tp), cut_hi = fmin(tf, tp);
+    if (sg > 0) {
+        lo[0] = tn; hi[0] = cut_hi; lo[1] = cut_lo; hi[1] = tf;
+    } else if (sg < 0) {
+        lo[0] = cut_lo; hi[0] = tf; lo[1] = tn; hi[1] = cut_hi;
+    } else {
+        const bool below = oa < p;
+        lo[0] = tn; hi[0] = below ? tf : tn; lo[1] = tn; hi[1] = below ? tn : tf;
+    }
+    return sg >= 0;
+}
+
 __device__ __forceinline__ int kd4_child(const Kd4Node& nd, int s) {
     return s < 2 ? (s == 0 ? nd.child[0] : nd.child[1]) : (s == 2 ? nd.child[2] : nd.child[3]);
 }
@@ -401,6 +438,8 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     __shared__ double s_tn[kWarpsPerBlock][32], s_tfar[kWarpsPerBlock][32];
     __shared__ SpillEnt s_stack[kWarpsPerBlock][kWarpStack];
     __shared__ SegQ s_q[kWarpsPerBlock][32];
+    __shared__ RayAxes s_ray[kWarpsPerBlock];
+    __shared__ BrickPart s_part[kFlatGather ? kWarpsPerBlock : 1][32];
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
     __syncthreads();
     const unsigned FULL = 0xffffffffu;
@@ -429,6 +468,15 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             int nreg = 0, nsmp = 0;
             if (tmin < tmax) {
                 if (ISO) tmax = A.iso_tend[slot];
+                RayAxes& rs = s_ray[wid];
+                __syncwarp();
+                if (lane < 3) {
+                    const double dl = sel3(lane, r.d);
+                    rs.o[lane] = sel3(lane, r.o);
+                    rs.inv[lane] = sel3(lane, r.inv);
+                    rs.sgn[lane] = dl > 0.0 ? 1 : (dl < 0.0 ? -1 : 0);
+                }
+                __syncwarp();
                 double t = tmin;  // the reference's query start (restart chain)
                 // ---- frontier: lane i < n holds list entry i; the rest is on the spill stack
                 int n = 0, spn = 0;
@@ -473,20 +521,27 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         const int s_end = __shfl_sync(FULL, q_P, sg);
                         double Ts = 1.0, Cs0 = 0.0, Cs1 = 0.0, Cs2 = 0.0;
                         unsigned long long my_bytes = 0;
+                        const int lev = sq.meta >> 24;
+                        const int nids = sq.meta & 0xffffff;
+                        double sl = 0.0, px = 0.0, py = 0.0, pz = 0.0;
                         if (act) {
-                            const int lev = sq.meta >> 24;
                             const double s_dt = A.M.lv_dt[lev];
                             const int j = s - (s_end - sq.cnt);
                             const double prev = j == 0 ? sq.ci : s_dt * ((sq.kf + (double)(j - 1)) + rho);
                             const double tk = j == sq.cnt - 1 ? sq.co : s_dt * ((sq.kf + (double)j) + rho);
-                            const double sl = tk - prev;
+                            sl = tk - prev;
                             const double mid = 0.5 * (prev + tk);
-                            const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1],
-                                         pz = r.o[2] + mid * r.d[2];
-                            const int nids = sq.meta & 0xffffff;
-                            const int32_t* ids = S.rids + sq.ids;
-                            FastAccum F;
-                            gather_shade<GRAD == 1>(S, ids, nids, px, py, pz, F);
+                            px = r.o[0] + mid * r.d[0];
+                            py = r.o[1] + mid * r.d[1];
+                            pz = r.o[2] + mid * r.d[2];
+                        }
+                        FastAccum F;
+                        if (kFlatGather) {
+                            gather_chunk<GRAD == 1>(S, act, sq.ids, nids, px, py, pz, s_part[wid], lane, F);
+                        } else if (act) {
+                            gather_shade<GRAD == 1>(S, S.rids + sq.ids, nids, px, py, pz, F);
+                        }
+                        if (act) {
                             if (COUNT) my_bytes = 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
                             if (F.den > kEpsWeight) {
                                 const double v = F.num / F.den;
@@ -501,8 +556,8 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                                         } else {
                                             double g[3];
                                             int64_t ne = 0;
-                                            central_gradient(S, A.M.grad_mode, px, py, pz, sq.rid, ids, nids, v, g,
-                                                             &ne);
+                                            central_gradient(S, A.M.grad_mode, px, py, pz, sq.rid, S.rids + sq.ids,
+                                                             nids, v, g, &ne);
                                             f = shade_factor(g, r);
                                         }
                                         c[0] *= f; c[1] *= f; c[2] *= f;
@@ -677,37 +732,41 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         continue;
                     }
                     // ---- expansion step: every unresolved entry is a Kd4 node; it is
-                    //      replaced in place by its (up to 4) surviving children, near first
+                    //      replaced in place by its (up to 4) surviving children, near
+                    //      first.  Branch-free: each split turns the entry interval into
+                    //      the intervals of its two sides with the same exact slab
+                    //      arithmetic as kd_next (an empty side gets lo >= hi).
                     bool actx = lane < n && e_code >= 0;
                     if (spn + 96 > kWarpStack) {  // near the spill limit: expand the first entry only
                         const unsigned um = __ballot_sync(FULL, actx);
                         actx = actx && lane == __ffs(um) - 1;
                     }
-                    int oc[4] = {0, 0, 0, 0};
-                    double otn[4] = {0.0, 0.0, 0.0, 0.0}, otf[4] = {0.0, 0.0, 0.0, 0.0};
-                    bool ov[4] = {false, false, false, false};  // candidate k: half k/2, child k%2
+                    int oc[4] = {e_code, 0, 0, 0};
+                    double otn[4] = {e_tn, 0.0, 0.0, 0.0}, otf[4] = {e_tf, 0.0, 0.0, 0.0};
+                    bool ov[4] = {lane < n && !actx, false, false, false};  // a resolved leaf stays in place
                     if (actx) {
                         const Kd4Node nd = S.kd4[e_code];
                         const uint32_t msk = A.vmask4[e_code];
-                        int hs[2] = {0, 0};
-                        double hn[2] = {0.0, 0.0}, hf[2] = {0.0, 0.0};
-                        int nh = 0;
+                        // first split: one or two halves, in ray order (kd_next's classification)
+                        int hs0 = 0, hs1 = 0, nh = 1;
+                        double hn0 = e_tn, hf0 = e_tf, hn1 = 0.0, hf1 = 0.0;
                         {
                             const int ax = nd.axes & 3;
                             const double p = (double)nd.plane[0] * 0.5;
-                            const double da = sel3(ax, r.d), oa = sel3(ax, r.o);
-                            if (da == 0.0) {
-                                hs[0] = oa < p ? 0 : 1; hn[0] = e_tn; hf[0] = e_tf; nh = 1;
+                            const int sg = rs.sgn[ax];
+                            const double oa = rs.o[ax];
+                            if (sg == 0) {
+                                hs0 = oa < p ? 0 : 1;
                             } else {
-                                const double tp = (p - oa) * sel3(ax, r.inv);
-                                const int ns_ = da > 0.0 ? 0 : 1;
+                                const double tp = (p - oa) * rs.inv[ax];
+                                const int ns_ = sg > 0 ? 0 : 1;
                                 if (tp >= e_tf) {
-                                    hs[0] = ns_; hn[0] = e_tn; hf[0] = e_tf; nh = 1;
+                                    hs0 = ns_;
                                 } else if (tp <= e_tn) {
-                                    hs[0] = 1 - ns_; hn[0] = e_tn; hf[0] = e_tf; nh = 1;
+                                    hs0 = 1 - ns_;
                                 } else {
-                                    hs[0] = ns_; hn[0] = e_tn; hf[0] = tp;
-                                    hs[1] = 1 - ns_; hn[1] = tp; hf[1] = e_tf;
+                                    hs0 = ns_; hf0 = tp;
+                                    hs1 = 1 - ns_; hn1 = tp; hf1 = e_tf;
                                     nh = 2;
                                 }
                             }
@@ -715,25 +774,27 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
 #pragma unroll
                         for (int h = 0; h < 2; h++) {
                             if (h < nh) {
-                                const int sd = hs[h];
+                                const int sd = h ? hs1 : hs0;
+                                const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
                                 const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
                                 int s0 = 2 * sd, s1 = -1;
-                                double a0 = hn[h], bb0 = hf[h], a1 = 0.0, bb1 = 0.0;
+                                double a0 = hn, bb0 = hf, a1 = 0.0, bb1 = 0.0;
                                 if (ax != 3) {
                                     const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
-                                    const double da = sel3(ax, r.d), oa = sel3(ax, r.o);
-                                    if (da == 0.0) {
+                                    const int sg = rs.sgn[ax];
+                                    const double oa = rs.o[ax];
+                                    if (sg == 0) {
                                         s0 = 2 * sd + (oa < p ? 0 : 1);
                                     } else {
-                                        const double tp = (p - oa) * sel3(ax, r.inv);
-                                        const int nqq = da > 0.0 ? 0 : 1;
+                                        const double tp = (p - oa) * rs.inv[ax];
+                                        const int nqq = sg > 0 ? 0 : 1;
                                         if (tp >= bb0) {
                                             s0 = 2 * sd + nqq;
                                         } else if (tp <= a0) {
                                             s0 = 2 * sd + 1 - nqq;
                                         } else {
                                             s0 = 2 * sd + nqq; bb0 = tp;
-                                            s1 = 2 * sd + 1 - nqq; a1 = tp; bb1 = hf[h];
+                                            s1 = 2 * sd + 1 - nqq; a1 = tp; bb1 = hf;
                                         }
                                     }
                                 }
@@ -744,9 +805,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                                 oc[2 * h + 1] = kd4_child(nd, s1 < 0 ? 0 : s1); otn[2 * h + 1] = a1; otf[2 * h + 1] = bb1;
                             }
                         }
-                    } else if (lane < n) {
-                        ov[0] = true;  // resolved leaf (behind the front): stays in place
-                        oc[0] = e_code; otn[0] = e_tn; otf[0] = e_tf;
                     }
                     const int cnt = (int)ov[0] + (int)ov[1] + (int)ov[2] + (int)ov[3];
                     const unsigned m1 = __ballot_sync(FULL, cnt & 1), m2 = __ballot_sync(FULL, cnt & 2),
