@@ -379,6 +379,13 @@ __device__ __forceinline__ double sel4(int i, const double v[4]) {
     return i < 2 ? (i == 0 ? v[0] : v[1]) : (i == 2 ? v[2] : v[3]);
 }
 
+// a set-up camera ray waiting for the warp (k_warp sets up 32 rays at once)
+struct RaySetup {
+    double d[3], inv[3];
+    double rho, tmin, tmax, a, b;  // jitter, clipped range (iso-bounded), root box interval
+    int64_t out;
+};
+
 // per-ray axis data in shared memory (one copy per warp)
 struct RayAxes {
     double o[3], inv[3];
@@ -439,6 +446,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     __shared__ SpillEnt s_stack[kWarpsPerBlock][kWarpStack];
     __shared__ SegQ s_q[kWarpsPerBlock][32];
     __shared__ RayAxes s_ray[kWarpsPerBlock];
+    __shared__ RaySetup s_setup[kWarpsPerBlock][32];
     __shared__ BrickPart s_part[kFlatGather ? kWarpsPerBlock : 1][32];
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
     __syncthreads();
@@ -451,23 +459,76 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     unsigned long long tot_reg = 0, tot_smp = 0, tot_bytes = 0;
 
     for (;;) {
+        // ---- 32 rays per grab: every lane sets up one ray (camera ray, jitter,
+        //      clip, root box); rays that reach no active region are written at
+        //      once, the others are marched one after another by the whole warp
+        //      Grab size: fixed 8 by default (C2 sweep, tools/ab.py: 32 -> 9.4 ms,
+        //      16 -> 7.9, 8 -> 7.7, 4 -> 7.9, 2 -> 8.4); XB_GRAB_FIXED=0 selects a
+        //      guided schedule (remaining / (grab_div x warps), clamped to [1, 32]).
         unsigned long long b0 = 0;
-        if (lane == 0) b0 = atomicAdd(A.work_counter, (unsigned long long)kRaysPerGrab);
+        int grab = 32;
+        if (lane == 0) {
+            const long long seen = (long long)*(volatile unsigned long long*)A.work_counter;
+            const long long left = (long long)n_slots - seen;
+            const long long g = left / ((long long)A.grab_div * gridDim.x * kWarpsPerBlock);
+            grab = A.grab_fixed > 0 ? A.grab_fixed : (int)max(1ll, min(32ll, g));
+            b0 = atomicAdd(A.work_counter, (unsigned long long)grab);
+        }
         b0 = __shfl_sync(FULL, b0, 0);
+        grab = __shfl_sync(FULL, grab, 0);
         if ((int64_t)b0 >= n_slots) break;
-        const int64_t b1 = min(n_slots, (int64_t)b0 + kRaysPerGrab);
-        for (int64_t slot = (int64_t)b0; slot < b1; slot++) {
-            const SlotPix sp = slot_pixel(A, slot);
-            if (!sp.live) continue;
+        const int64_t my_slot = (int64_t)b0 + lane;
+        SlotPix msp = slot_pixel(A, my_slot);
+        msp.live = msp.live && lane < grab && my_slot < n_slots;
+        Ray mr;
+        pixel_ray(A, msp.x, msp.y, mr);
+        const double my_rho = rho_hash((uint64_t)msp.pix, A.M.seed);
+        double my_tmin = 0.0, my_tmax = kTFar;
+        clip_ray(A.M, mr, my_tmin, my_tmax);
+        const bool my_clip_ok = msp.live && my_tmin < my_tmax;
+        if (ISO && my_clip_ok) my_tmax = A.iso_tend[my_slot];
+        double my_a = 0.0, my_b = -1.0;
+        slab_h(S.root_lo, S.root_hi, mr, my_a, my_b);
+        const bool my_has = my_clip_ok && S.n_kd > 0 && my_a <= my_b && A.vflags[0];
+        if (msp.live && !my_has) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (ISO && my_clip_ok) {
+                const double f = A.iso_shade[my_slot];
+                if (f >= 0.0) {
+                    acc[0] = A.M.iso_rgb[0] * f;
+                    acc[1] = A.M.iso_rgb[1] * f;
+                    acc[2] = A.M.iso_rgb[2] * f;
+                    acc[3] = 1.0;
+                }
+            }
+            write_pixel(A, msp.out, acc, 0, 0);
+        }
+        unsigned todo = __ballot_sync(FULL, my_has);  // (also orders the previous batch's reads)
+        if (my_has) {  // park the ray in shared memory until its turn
+            RaySetup& q = s_setup[wid][lane];
+            q.d[0] = mr.d[0]; q.d[1] = mr.d[1]; q.d[2] = mr.d[2];
+            q.inv[0] = mr.inv[0]; q.inv[1] = mr.inv[1]; q.inv[2] = mr.inv[2];
+            q.rho = my_rho; q.tmin = my_tmin; q.tmax = my_tmax; q.a = my_a; q.b = my_b;
+            q.out = msp.out;
+        }
+        __syncwarp();
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const RaySetup& q = s_setup[wid][src];
             Ray r;
-            pixel_ray(A, sp.x, sp.y, r);
-            const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
-            double tmin = 0.0, tmax = kTFar;
-            clip_ray(A.M, r, tmin, tmax);
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                r.o[a] = A.pos[a];
+                r.d[a] = q.d[a];
+                r.inv[a] = q.inv[a];
+            }
+            const double rho = q.rho, tmin = q.tmin, tmax = q.tmax, root_a = q.a, root_b = q.b;
+            const int64_t slot = (int64_t)b0 + src;
+            const int64_t out_px = q.out;
             double Tr = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;  // transmittance, premultiplied colour
             int nreg = 0, nsmp = 0;
-            if (tmin < tmax) {
-                if (ISO) tmax = A.iso_tend[slot];
+            {
                 RayAxes& rs = s_ray[wid];
                 __syncwarp();
                 if (lane < 3) {
@@ -482,18 +543,11 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                 int n = 0, spn = 0;
                 int e_code = -1;
                 double e_tn = 0.0, e_tf = 0.0;
-                {
-                    double a, b;
-                    slab_h(S.root_lo, S.root_hi, r, a, b);
-                    if (S.n_kd > 0 && a <= b && A.vflags[0]) {
-                        n = 1;
-                        if (lane == 0) {
-                            // Kd4 node 0 is the binary root when it is interior; a leaf root resolves at once
-                            e_code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
-                            e_tn = a;
-                            e_tf = b;
-                        }
-                    }
+                n = 1;  // the root: Kd4 node 0 when the binary root is interior, else a leaf resolved at once
+                if (lane == 0) {
+                    e_code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
+                    e_tn = root_a;
+                    e_tf = root_b;
                 }
                 bool walk = n > 0;
                 // ---- segment queue: lane i < nq holds visited region i (in ray order)
@@ -842,7 +896,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             }
             if (lane == 0) {
                 double acc[4] = {Cr, Cg, Cb, 1.0 - Tr};
-                if (ISO && tmin < tmax) {
+                if (ISO) {
                     const double f = A.iso_shade[slot];
                     if (f >= 0.0) {
                         const double wgt = 1.0 - acc[3];
@@ -852,7 +906,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         acc[3] = 1.0;
                     }
                 }
-                write_pixel(A, sp.out, acc, nreg, nsmp);
+                write_pixel(A, out_px, acc, nreg, nsmp);
                 tot_reg += nreg;
                 tot_smp += nsmp;
             }
@@ -962,6 +1016,11 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         XB_CUDA(cudaLaunchKernel(fn, dim3(grid_for(n_slots, 128)), dim3(128), args, 0, s));
     }
     const int kc = kernel_choice();
+    {  // k_warp guided ray-grab schedule (tuning knob XB_GRAB_DIV)
+        RenderArgs& W = const_cast<RenderArgs&>(A);
+        W.grab_div = getenv("XB_GRAB_DIV") ? std::max(1, atoi(getenv("XB_GRAB_DIV"))) : 4;
+        W.grab_fixed = getenv("XB_GRAB_FIXED") ? std::min(32, atoi(getenv("XB_GRAB_FIXED"))) : 8;
+    }
     if (kc == 2) {
         RenderFn fn;
         if (g == 0) fn = iso ? tile_fn<0, true>(count) : tile_fn<0, false>(count);

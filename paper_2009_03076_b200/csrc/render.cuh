@@ -25,7 +25,8 @@ struct RenderArgs {
     double4* outf;
     int2* outcnt;
     unsigned long long* stats;  // [regions, samples, algorithmic bytes]
-    unsigned long long* work_counter;  // k_frame slot counter (zeroed per launch)
+    unsigned long long* work_counter;  // k_frame / k_warp slot counter (zeroed per launch)
+    int grab_div, grab_fixed;          // k_warp grab schedule (launch_render)
     double* iso_tend;           // per slot: volume t_end (iso hit or clip end)
     double* iso_shade;          // per slot: headlight factor of the iso hit, < 0 when none
     double tf[1024];

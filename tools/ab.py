@@ -29,10 +29,14 @@ stream = torch.cuda.current_stream()
 
 
 def setv(v):
-    """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N)"""
-    os.environ.pop("XB_KERNEL", None)
-    os.environ.pop("XB_WMINB", None)
-    if v.startswith("warp") and len(v) > 4:
+    """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N) | gD (guided grab divisor D)"""
+    for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED"):
+        os.environ.pop(k, None)
+    if v.startswith("f") and v[1:].isdigit():
+        os.environ["XB_GRAB_FIXED"] = v[1:]
+    elif v.startswith("g") and v[1:].isdigit():
+        os.environ["XB_GRAB_DIV"] = v[1:]
+    elif v.startswith("warp") and len(v) > 4:
         os.environ["XB_WMINB"] = v[4:]
     elif v != "warp":
         os.environ["XB_KERNEL"] = v
