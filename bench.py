@@ -408,7 +408,7 @@ def bench_ours(args, cfg):
             "kernel_ms": ms_kernel, "wall_s_timed": wall,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_render<1,false,false> (csrc/render.cu)",
+                         "kernel": "k_warp<1,false,false> (csrc/render.cu)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6.65 TB/s"},
             "gpu_launches": args.steps * (1 if world == 1 else 2),
             "e2e": e2e,

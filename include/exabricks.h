@@ -38,6 +38,7 @@ extern "C" {
 #define XB_ERR_NO_TREE (-5)
 #define XB_ERR_INTERNAL (-6)
 
+typedef struct xb_cells xb_cells;     /* CellList on the device (R/model.py:124-205) */
 typedef struct xb_model xb_model;     /* AmrModel on the device (R/model.py:250-343) */
 typedef struct xb_regions xb_regions; /* RegionSet + its k-d tree (R/regions.py:35-79) */
 typedef struct xb_active xb_active;   /* pruned region set = RegionBvh (R/accel.py:125-155) */
@@ -46,8 +47,33 @@ const char* xb_last_error(void);
 int xb_abi_version(void);
 int xb_device_count(int32_t* n);
 
+/* ---- synthetic inputs: generate_synthetic(SyntheticSpec) R/io.py:198-295 ---- */
+typedef struct {
+    int32_t field;     /* 0 gaussian, 1 ramp, 2 constant, 3 octaves (make_field, R/io.py:221-235) */
+    int32_t max_level;
+    int64_t extent[3]; /* finest-cell units, multiples of 2**max_level */
+    double threshold;  /* split when |grad f(centre)| * width >= threshold */
+    int32_t n_holes, n_refine;
+    double holes[32][4];  /* (cx, cy, cz, r): emitted cells with centre inside are dropped */
+    double refine[32][4]; /* (cx, cy, cz, r): cells with centre inside always split */
+    double center[3], sigma, amp;  /* GaussianField */
+    double direction[3], offset;   /* RampField */
+    double constant;               /* ConstantField */
+    int32_t n_waves;               /* OctaveField: waves drawn on the host with the reference's RNG */
+    double waves[8][5];            /* k[3], phase, amplitude */
+} xb_synth_spec;
+
+/* The cells stay on `device` (10^8-10^9 cells build without a host round trip). */
+int xb_generate_synthetic(const xb_synth_spec* spec, int32_t device, xb_cells** out);
+int xb_cells_info(const xb_cells* c, int64_t* n);
+/* host arrays of length n: CellList.i/j/k/level (int32) and values (float32, one field) */
+int xb_cells_download(const xb_cells* c, int32_t* i, int32_t* j, int32_t* k, int32_t* level, float* values);
+void xb_cells_free(xb_cells* c);
+/* build_bricks on device-resident cells (same result as xb_build_bricks on the downloaded arrays) */
+int xb_build_bricks_cells(const xb_cells* c, int32_t max_brick_width, int32_t keep_split_tree, xb_model** out);
+
 /* ---- bricks: build_bricks(cells, BrickBuildParams) R/bricks.py:104-228 ---- */
-/* values: (n, n_fields) row-major float32, as CellList.values (R/model.py:135-138).
+/* values: (n, n_fields) row-major float32, as CellList.values (R/model.py:135-138); host or device pointers.
  * XB_ERR_INVALID_CELLS when validate_cells (R/model.py:392-457) would fail. */
 int xb_build_bricks(const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* level, const float* values,
                     int64_t n, int32_t n_fields, int32_t max_brick_width, int32_t keep_split_tree, int32_t device,

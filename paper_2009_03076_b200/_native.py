@@ -45,11 +45,23 @@ class XbMarch(C.Structure):
                 ("iso_value", f64), ("iso_rgb", f64 * 3), ("tf_lo", f64), ("tf_hi", f64), ("tf_rgba", f64 * 1024)]
 
 
+class XbSynthSpec(C.Structure):
+    _fields_ = [("field", i32), ("max_level", i32), ("extent", i64 * 3), ("threshold", f64), ("n_holes", i32),
+                ("n_refine", i32), ("holes", (f64 * 4) * 32), ("refine", (f64 * 4) * 32), ("center", f64 * 3),
+                ("sigma", f64), ("amp", f64), ("direction", f64 * 3), ("offset", f64), ("constant", f64),
+                ("n_waves", i32), ("waves", (f64 * 5) * 8)]
+
+
 # exported symbol -> (restype, argtypes); tests check every declared symbol
 SIGNATURES = {
     "xb_last_error": (C.c_char_p, []),
     "xb_abi_version": (C.c_int, []),
     "xb_device_count": (C.c_int, [P]),
+    "xb_generate_synthetic": (C.c_int, [P, i32, P]),
+    "xb_cells_info": (C.c_int, [P, P]),
+    "xb_cells_download": (C.c_int, [P, P, P, P, P, P]),
+    "xb_cells_free": (None, [P]),
+    "xb_build_bricks_cells": (C.c_int, [P, i32, i32, P]),
     "xb_build_bricks": (C.c_int, [P, P, P, P, P, i64, i32, i32, i32, i32, P]),
     "xb_model_upload": (C.c_int, [P, P, P, P, i64, i64, i32, i32, P]),
     "xb_model_info": (C.c_int, [P, P, P, P, P]),
@@ -160,6 +172,10 @@ class Handle:
         if h and self._free and _lib is not None:
             getattr(_lib, self._free)(h)
             self.h = None
+
+
+class CellsHandle(Handle):
+    _free = "xb_cells_free"
 
 
 class ModelHandle(Handle):

@@ -70,6 +70,19 @@ def build_bricks(cells, params: BrickBuildParams | None = None):
     permutation (cells are canonically ordered by (level, k, j, i) first).
     """
     params = params or BrickBuildParams()
+    from .io import DeviceCells
+
+    if isinstance(cells, DeviceCells):  # GPU-resident cells (generate_synthetic_device)
+        L = N.lib()
+        h = N.new_handle()
+        N.check(L.xb_build_bricks_cells(cells.handle.h, int(min(params.max_brick_width, 2**31 - 1)),
+                                        int(params.keep_split_tree), C.byref(h)))
+        mh = N.ModelHandle(h.value, cells.handle.device)
+        model = model_from_handle(mh, cells.field_names)
+        tree = None
+        if params.keep_split_tree:
+            tree = tree_from_handle(mh) if len(cells) else _empty_tree()
+        return model, tree
     cl = _as_cell_list(cells)
     names = cl.field_names
     dev = N.require_device()

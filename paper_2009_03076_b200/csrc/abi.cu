@@ -6,6 +6,7 @@
 #include "../../include/exabricks.h"
 #include "accel.cuh"
 #include "render.cuh"
+#include "synth.cuh"
 
 namespace xb {
 bool build_bricks_device(const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* l, const float* v,
@@ -14,6 +15,9 @@ void finish_model(DevModel& m, cudaStream_t s);
 void build_regions_device(const DevModel& m, DevRegions& out, cudaStream_t s);
 }  // namespace xb
 
+struct xb_cells {
+    xb::DevCells c;
+};
 struct xb_model {
     xb::DevModel m;
 };
@@ -183,6 +187,56 @@ int xb_build_bricks(const int32_t* i, const int32_t* j, const int32_t* k, const 
         auto h = std::make_unique<xb_model>();
         bool ok = xb::build_bricks_device(i, j, k, level, values, n, n_fields, max_brick_width, keep_split_tree != 0,
                                           device, h->m, st.s);
+        XB_CHECK(ok, XB_ERR_INVALID_CELLS, "cells fail validation (alignment, duplicates or overlaps)");
+        *out = h.release();
+    });
+}
+
+int xb_generate_synthetic(const xb_synth_spec* spec, int32_t device, xb_cells** out) {
+    *out = nullptr;
+    return guarded([&] {
+        XB_CHECK(spec != nullptr, XB_ERR_ARG, "null spec");
+        xb::DeviceGuard g(device);
+        OwnedStream st;
+        auto h = std::make_unique<xb_cells>();
+        xb::generate_synthetic_device(*spec, device, h->c, st.s);
+        *out = h.release();
+    });
+}
+
+int xb_cells_info(const xb_cells* c, int64_t* n) {
+    return guarded([&] {
+        XB_CHECK(c && n, XB_ERR_ARG, "null argument");
+        *n = c->c.n;
+    });
+}
+
+int xb_cells_download(const xb_cells* c, int32_t* i, int32_t* j, int32_t* k, int32_t* level, float* values) {
+    return guarded([&] {
+        XB_CHECK(c != nullptr, XB_ERR_ARG, "null cells");
+        xb::DeviceGuard g(c->c.device);
+        OwnedStream st;
+        const size_t n = (size_t)c->c.n;
+        if (i) c->c.i.download(i, n, st.s);
+        if (j) c->c.j.download(j, n, st.s);
+        if (k) c->c.k.download(k, n, st.s);
+        if (level) c->c.level.download(level, n, st.s);
+        if (values) c->c.vals.download(values, n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+void xb_cells_free(xb_cells* c) { delete c; }
+
+int xb_build_bricks_cells(const xb_cells* c, int32_t max_brick_width, int32_t keep_split_tree, xb_model** out) {
+    *out = nullptr;
+    return guarded([&] {
+        XB_CHECK(c != nullptr, XB_ERR_ARG, "null cells");
+        xb::DeviceGuard g(c->c.device);
+        OwnedStream st;
+        auto h = std::make_unique<xb_model>();
+        bool ok = xb::build_bricks_device(c->c.i.p, c->c.j.p, c->c.k.p, c->c.level.p, c->c.vals.p, c->c.n, 1,
+                                          max_brick_width, keep_split_tree != 0, c->c.device, h->m, st.s);
         XB_CHECK(ok, XB_ERR_INVALID_CELLS, "cells fail validation (alignment, duplicates or overlaps)");
         *out = h.release();
     });

@@ -81,9 +81,9 @@ struct DevBuf {
         p = nullptr;
         n = 0;
     }
-    void upload(const T* h, size_t count, cudaStream_t s = 0) {
+    void upload(const T* h, size_t count, cudaStream_t s = 0) {  // h: host or device (UVA)
         if (count > n) alloc(count);
-        if (count) XB_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (count) XB_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyDefault, s));
     }
     void download(T* h, size_t count, cudaStream_t s = 0) const {
         if (count) XB_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, s));
