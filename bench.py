@@ -1,15 +1,18 @@
 #!/usr/bin/env python
 """bench.py — ExaBricks render hot path on B200 (one JSON line on rank 0).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c2]
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config c3] [--secondary c2]
 
-Workload (N=1): BASELINE.json configs[1] — synthetic 4-level gaussian AMR
-(9.53M cells, SURVEY.md §8(d) "C2"), DVR + analytic-gradient shading,
-grayscale TF (max alpha 0.5), 1024x1024, orbit view 0, seed 0.  A step is one
-frame: ray march of every pixel through the resident scene (+ the NCCL tile
-gather for N>1).  Inputs are resident in HBM; L2 (126 MB) is flushed by a
-256 MB write between timed frames.  Metric: frames/s (whole job) with
-Msamples/s beside it (`FrameStats.samples` / s, R/render.py:419).
+Workload (N=1): BASELINE.json configs[2], the configuration the metric ("at
+1920x1080") is quoted on — a synthetic Landing-Gear-shaped AMR volume (13
+levels, 4096:1, 266M cells, SURVEY.md §8(d) "C3") generated on the GPU, DVR +
+analytic-gradient shading, grayscale TF (max alpha 0.5), 1920x1080, orbit view
+0, seed 0.  configs[1] ("C2": 9.53M cells, 1024x1024) is timed in the same run
+and reported under "secondary".  A step is one frame: ray march of every pixel
+through the resident scene (+ the NCCL tile gather for N>1).  Inputs are
+resident in HBM; L2 (126 MB) is flushed by a 256 MB write between timed frames.
+Metric: frames/s (whole job) with Msamples/s beside it (`FrameStats.samples`
+/ s, R/render.py:419).
 
 `--impl reference` times the CPU oracle port (oracle/, a C restatement of the
 reference renderer, all host threads) on bounded row samples of the same frame.
@@ -45,7 +48,39 @@ CONFIGS = {
     "c2_1080p": dict(spec=dict(field="gaussian", extent=(256, 256, 256), max_level=3, threshold=0.004, seed=0),
                      res=(1920, 1080), max_alpha=0.5, gradient="analytic",
                      workload="configs[1] model at 1920x1080, DVR + analytic gradient shading"),
+    # Landing-Gear-shaped, 12 refinement steps (4096:1), hole + level-0 shell,
+    # 266,139,607 cells (R_h 200, R_r 420), generated on the GPU (csrc/synth.cu)
+    "c3": dict(spec=dict(field="gaussian", extent=(16384, 8192, 8192), max_level=12, threshold=0.05, seed=0,
+                         holes=((6144.0, 6144.0, 6144.0, 200.0),), refine_spheres=((6144.0, 6144.0, 6144.0, 420.0),),
+                         field_params={"center": (6144.0, 6144.0, 6144.0), "sigma": 600.0}),
+               gpu_gen=True, res=(1920, 1080), max_alpha=0.5, gradient="analytic",
+               workload="configs[2]: synthetic Landing-Gear-shaped AMR (13 levels, 4096:1 cell ratio, 266M cells), "
+                        "1920x1080 DVR + analytic gradient shading, 1 GPU"),
+    # C4: C3 + implicit iso-surface (0.5) + DVR, and a timed TF-edit majorant refresh
+    "c4": dict(spec="c3", gpu_gen=True, res=(1920, 1080), max_alpha=0.5, gradient="analytic", iso=0.5,
+               workload="configs[3]: Landing-Gear-shaped AMR (266M cells), implicit iso-surface 0.5 + DVR, "
+                        "1920x1080, with a TF-edit active-set/majorant refresh"),
+    # C5: Exajet-shaped, 4 levels, hole/refine chain along x (SURVEY.md §8(d) template)
+    "c5": dict(spec="jet", gpu_gen=True, res=(1920, 1080), max_alpha=0.5, gradient="analytic",
+               workload="configs[4]: synthetic Exajet-shaped AMR (4 levels), 1920x1080 DVR + analytic shading"),
 }
+JET = dict(thr=0.0027, rh=80.0, rr=240.0, step=80.0, sigma=400.0)
+
+
+def spec_for(cfg):
+    from paper_2009_03076_b200 import io as xio
+
+    sp = cfg["spec"]
+    if sp == "c3":
+        sp = CONFIGS["c3"]["spec"]
+    if sp == "jet":
+        X, Y, Z = 2048, 1024, 1024
+        xs = np.arange(0.2 * X, 0.8 * X + 1e-9, JET["step"])
+        return xio.SyntheticSpec(field="gaussian", extent=(X, Y, Z), max_level=3, threshold=JET["thr"], seed=0,
+                                 holes=tuple((float(x), Y / 2, Z / 2, JET["rh"]) for x in xs),
+                                 refine_spheres=tuple((float(x), Y / 2, Z / 2, JET["rr"]) for x in xs),
+                                 field_params={"center": (X / 2, Y / 2, Z / 2), "sigma": JET["sigma"]})
+    return xio.SyntheticSpec(**sp)
 
 
 def parse():
@@ -54,7 +89,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--secondary", default="c2", help="second config timed in the same run ('' = none)")
     ap.add_argument("--view", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -70,10 +106,16 @@ def log(*a):
 # workload
 
 
-def make_cells(cfg):
+def make_cells(cfg, host=False):
+    """Synthetic cells of a config: numpy generator (C1/C2) or the GPU generator
+    (C3-C5, left on the device unless `host`)."""
     from paper_2009_03076_b200 import io as xio
 
-    return xio.generate_synthetic(xio.SyntheticSpec(**cfg["spec"]))
+    spec = spec_for(cfg)
+    if cfg.get("gpu_gen"):
+        dc = xio.generate_synthetic_device(spec)
+        return dc.to_host() if host else dc
+    return xio.generate_synthetic(spec)
 
 
 def camera_for(bounds, cfg, view):
@@ -94,60 +136,64 @@ def tf_for(vr, cfg):
 
 
 class ClockSampler:
-    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons polled every ~2 ms through NVML (the
+    nvidia-smi fields clocks.sm / clocks_event_reasons.*) while the timed frames
+    run; falls back to `nvidia-smi -lms 100` when NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4))
 
     def __init__(self, device):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (sm_mhz, reason bits)
+        self.max_mhz = None
+        self.stop = threading.Event()
+        self.t = None
+        self.nv = None
+
+    def _handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(self.device)
+        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
-                text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.nv, h = self._handle()
+            self.max_mhz = float(self.nv.nvmlDeviceGetMaxClockInfo(h, self.nv.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = float(self.nv.nvmlDeviceGetClockInfo(h, self.nv.NVML_CLOCK_SM))
+                        rs = int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                        self.samples.append((sm, rs))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
             self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) != len(self.FIELDS):
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
-        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "source": "nvml"}
+        sm = [x for x, _ in self.samples]
+        reasons = sorted({n for _, bits in self.samples for n, b in self.REASONS if bits & b})
+        loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "source": "nvml 2 ms poll"}
 
 
 # ---------------------------------------------------------------------------
@@ -160,7 +206,7 @@ def oracle_scene_from(model_arrays, region_arrays):
     return oracle.OracleScene(model_arrays, region_arrays)
 
 
-def cpu_rate(osc, cam, tf, params, W, H, target_s, threads):
+def cpu_rate(osc, cam, tf, params, W, H, target_s, threads, iso=None):
     """Render bounded row bands spread over the frame until ~target_s of CPU work.
     Returns (Msamples/s, frames/s-equivalent, sample description)."""
     import oracle
@@ -168,6 +214,7 @@ def cpu_rate(osc, cam, tf, params, W, H, target_s, threads):
     r, u, f = cam.basis()
     ocam = oracle.camera_struct(W, H, cam.position, r, u, f, math.tan(math.radians(cam.fov_y) * 0.5), W / H)
     osc.set_tf(tf.domain, tf.rgba)
+    osc.set_iso(iso)
     kw = dict(seed=params.seed, gradient_mode=params.gradient_mode, early=params.early_term_threshold,
               spc=params.samples_per_cell, rate=params.rate_scale)
     # probe: 8 rows spread over the frame
@@ -201,7 +248,7 @@ def bench_reference(args, cfg):
     import oracle
     from paper_2009_03076_b200.render import MarchParams
 
-    cells = make_cells(cfg)
+    cells = make_cells(cfg, host=True)  # C3-C5: GPU generator, bit-exact to the reference generator's digests
     t0 = time.perf_counter()
     m = oracle.build_bricks(cells.i, cells.j, cells.k, cells.level, cells.values)
     r = oracle.build_regions(m["brick_lower"], m["brick_level"], m["brick_dims"], m["brick_offset"], m["scalars"])
@@ -217,10 +264,10 @@ def bench_reference(args, cfg):
     W, H = cfg["res"]
     per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
-        cpu_rate(osc, cam, tf, params, W, H, per_step / 4, threads)
+        cpu_rate(osc, cam, tf, params, W, H, per_step / 4, threads, iso=cfg.get("iso"))
     rates, fps, desc, total = [], [], "", 0.0
     for _ in range(args.steps):
-        ms, fs, desc, dt = cpu_rate(osc, cam, tf, params, W, H, per_step, threads)
+        ms, fs, desc, dt = cpu_rate(osc, cam, tf, params, W, H, per_step, threads, iso=cfg.get("iso"))
         rates.append(ms)
         fps.append(fs)
         total += dt
@@ -250,6 +297,29 @@ def bench_ours(args, cfg):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = run_config(args, cfg, args.config, with_extras=True)
+    if line is not None and args.secondary and args.secondary != args.config:
+        sec = run_config(args, CONFIGS[args.secondary], args.secondary, with_extras=False)
+        line["secondary"] = {k: sec[k] for k in ("value", "unit", "ms_per_step", "msamples_per_s", "frame",
+                                                 "kernel_ms", "roofline")}
+        line["secondary"]["config"] = sec["config"]
+    elif args.secondary and args.secondary != args.config:
+        run_config(args, CONFIGS[args.secondary], args.secondary, with_extras=False)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_config(args, cfg, cfg_name, with_extras):
+    """Build the scene of `cfg`, time args.steps frames; returns rank 0's JSON
+    dict (None elsewhere).  with_extras: e2e, CPU baseline and clocks too."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", local)
 
     from paper_2009_03076_b200 import _native as N
@@ -261,18 +331,34 @@ def bench_ours(args, cfg):
     N.require_device(local)
     cells = make_cells(cfg)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    t0 = time.perf_counter()  # build times exclude cell generation
     model, _ = build_bricks(cells)
     t1 = time.perf_counter()
     regions = build_regions(model)
     t2 = time.perf_counter()
     tf = tf_for(model.value_range(0), cfg)
-    scene = build_scene(model, regions, tf)
+    scene = build_scene(model, regions, tf, iso_value=cfg.get("iso"))
     t3 = time.perf_counter()
+    tf_refresh_ms = None
+    if cfg.get("iso") is not None:
+        # config 4's interactive TF edit: rebuild the volume active set (majorants) for a new ramp
+        from paper_2009_03076_b200.accel import build_volume_bvh
+
+        tf2 = tf_for(model.value_range(0), dict(cfg, max_alpha=0.3))
+        build_volume_bvh(regions, tf2, 0, model=model)
+        reps = []
+        for _ in range(5):
+            torch.cuda.synchronize()
+            ta = time.perf_counter()
+            build_volume_bvh(regions, tf2, 0, model=model)
+            reps.append((time.perf_counter() - ta) * 1e3)
+        tf_refresh_ms = float(np.median(reps))
     W, H = cfg["res"]
     cam = camera_for(regions.bounds, cfg, args.view)
     params = MarchParams(seed=0, gradient_mode=cfg["gradient"])
     rend = TiledRenderer(scene, W, H, dev)
+    n_cells = len(cells)
+    del cells  # device cells are not needed after the build
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     # algorithmic bytes + counters of this rank's share (one untimed counting launch)
@@ -295,7 +381,7 @@ def bench_ours(args, cfg):
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local) if not args.profile else None
+    sampler = ClockSampler(local) if (with_extras and not args.profile) else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -332,7 +418,7 @@ def bench_ours(args, cfg):
 
     # ---- e2e through the public API: host output, stats read back every frame
     e2e = None
-    if not args.profile:
+    if with_extras and not args.profile:
         if world == 1:
             render_frame(scene, cam, tf, params)
             torch.cuda.synchronize()
@@ -374,18 +460,18 @@ def bench_ours(args, cfg):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = bytes_pf / (float(kern_ms.mean()) * 1e-3) / 1e9  # this rank's launch
     traffic = None
-    tp = ROOT / "profiles" / f"traffic_{args.config}.json"
+    tp = ROOT / "profiles" / f"traffic_{cfg_name}.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+    if with_extras and rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         osc = oracle_scene_from({k: getattr(model, k) for k in ("brick_lower", "brick_level", "brick_dims",
                                                                 "brick_offset", "scalars")},
                                 {k: getattr(regions, k) for k in ("lo", "hi", "brick_off", "brick_ids",
                                                                   "value_range", "finest_width")})
         threads = os.cpu_count() or 1
-        ms_, fs_, desc, dt = cpu_rate(osc, cam, tf, params, W, H, args.cpu_seconds, threads)
+        ms_, fs_, desc, dt = cpu_rate(osc, cam, tf, params, W, H, args.cpu_seconds, threads, iso=cfg.get("iso"))
         cpu = {"value": fs_, "unit": "frames/s", "cores": threads, "kind": "port",
                "sample": desc + " (oracle/xb_oracle.c, OpenMP, GPU-built bit-exact arrays)",
                "msamples_per_s": ms_}
@@ -397,11 +483,13 @@ def bench_ours(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "width": W, "height": H, "view": args.view,
-                       "cells": int(model.n_cells), "bricks": int(model.n_bricks), "regions": int(len(regions)),
+                       "cells": int(n_cells), "bricks": int(model.n_bricks), "regions": int(len(regions)),
                        "gradient_mode": cfg["gradient"], "tf": f"grayscale max_alpha={cfg['max_alpha']}",
                        "l2": "flushed between frames (256 MB write)", "parallelism": f"screen tiles 16x8 x{world}",
                        "build_ms": {"bricks": round((t1 - t0) * 1e3, 1), "regions": round((t2 - t1) * 1e3, 1),
-                                    "tf_active_sets": round((t3 - t2) * 1e3, 1)}},
+                                    "tf_active_sets": round((t3 - t2) * 1e3, 1)},
+                       "iso_value": cfg.get("iso"), "tf_refresh_ms": tf_refresh_ms,
+                       "cells_source": "GPU generator (csrc/synth.cu)" if cfg.get("gpu_gen") else "numpy generator"},
             "msamples_per_s": tot_samples / (ms_step * 1e-3) / 1e6,
             "frame": {"samples": tot_samples, "region_visits": tot_regions, "alg_bytes": tot_bytes,
                       "alg_bytes_per_sample": tot_bytes / max(tot_samples, 1)},
@@ -410,15 +498,15 @@ def bench_ours(args, cfg):
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_warp<1,false,false> (csrc/render.cu)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6.65 TB/s"},
-            "gpu_launches": args.steps * (1 if world == 1 else 2),
+            # our kernels per frame: k_warp (+ k_iso_pass) (+ k_unpack_tiles on rank 0 when tiled)
+            "gpu_launches": args.steps * (1 + (cfg.get("iso") is not None) + (world > 1)),
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
         if sampler:
             line["clocks"] = sampler.summary()
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+        return line
+    return None
 
 
 def main():

@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_synth.py -q -m gpu -x --timeout 600 > gpurun_out/pt_synth1.log 2>&1; tail -15 gpurun_out/pt_synth1.log
+timeout 900 python bench.py > gpurun_out/bench_def.json 2> gpurun_out/bench_def.err; tail -c 2500 gpurun_out/bench_def.json; tail -3 gpurun_out/bench_def.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 1500 gpurun_out/bench_ref.json; tail -3 gpurun_out/bench_ref.err
