@@ -1,6 +1,7 @@
 // abi.cu — extern "C" entry points of libexabricks (include/exabricks.h).
 #include <cmath>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include "../../include/exabricks.h"
@@ -69,6 +70,19 @@ struct OwnedStream {
         if (s) cudaStreamDestroy(s);
     }
 };
+
+// keep freed stream-ordered allocations in the device pool (per-frame scratch
+// of up to a few GB is reused every frame instead of going back to the driver)
+void keep_pool(int device) {
+    static bool done[64] = {};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
+}
 
 xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     XB_CHECK(m && r, XB_ERR_ARG, "null model or regions");
@@ -453,6 +467,7 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         check_active(vol, r, "volume");
         A->vflags = vol->a.flags.p;
         A->vmask4 = vol->a.mask4.p;
+        A->vqmin = vol->a.qmin.n ? vol->a.qmin.p : nullptr;
         fill_march(A->M, mp);
         A->M.iso_on = (mp->iso_on && iso) ? 1 : 0;
         if (A->M.iso_on) check_active(iso, r, "iso");
@@ -485,10 +500,11 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->out8 = o8.dev;
         A->outf = of.dev;
         A->outcnt = oc.dev;
-        // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter]
+        // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter, walk counter, hits]
         unsigned long long* scratch = nullptr;
-        XB_CUDA(cudaMallocAsync((void**)&scratch, 4 * sizeof(unsigned long long), s));
-        XB_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMallocAsync((void**)&scratch, 6 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMemsetAsync(scratch, 0, 6 * sizeof(unsigned long long), s));
+        A->walk_counter = scratch + 4;
         unsigned long long* dstats = (stats || count_bytes) ? scratch : nullptr;
         A->stats = dstats;
         A->work_counter = scratch + 3;
@@ -499,7 +515,31 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             A->iso_tend = iso_buf;
             A->iso_shade = iso_buf + n_slots;
         }
+        // k_walk -> k_warp leaf lists (the default warp kernel; XB_WALK=0 or another
+        // XB_KERNEL runs the frontier-only path)
+        int32_t* leaf_buf = nullptr;
+        A->leaves = nullptr;
+        A->leaf_count = nullptr;
+        A->leaf_cap = 0;
+        {
+            const char* ek = getenv("XB_KERNEL");
+            const char* ew = getenv("XB_WALK");
+            const bool walk = !(ek && (strcmp(ek, "frame") == 0 || strcmp(ek, "tile") == 0)) && !(ew && ew[0] == '0');
+            if (walk) {
+                keep_pool(m->m.device);
+                const char* ec = getenv("XB_LEAF_CAP");
+                const int cap = ec ? std::max(1, atoi(ec)) : 64;  // sweep: C2 64 ~ 128 ~ 384, C3 16 < 32 < 64 << 384
+                const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
+                const size_t ns1 = std::max<size_t>(n_slots, 1);
+                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 2) * sizeof(int32_t), s));
+                A->leaf_count = leaf_buf;
+                A->hit_list = leaf_buf + ns1;
+                A->leaves = leaf_buf + 2 * ns1;
+                A->leaf_cap = cap;
+            }
+        }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
+        if (leaf_buf) XB_CUDA(cudaFreeAsync(leaf_buf, s));
         if (iso_buf) XB_CUDA(cudaFreeAsync(iso_buf, s));
         o8.finish();
         of.finish();

@@ -43,6 +43,38 @@ struct AlphaTab {
     double a[256];
 };
 
+// Opacity minorant of a region for the walk's early-stop heuristic
+// (render.cu:k_walk): the minimum of the TF alpha ramp over the region's
+// value range, expressed as optical depth per unit ray length at spc = 1,
+// q = -log(1 - a_min) / finest_width, so the opacity after a length L inside
+// the region is at least 1 - exp(-spc * q * L) (R/render.py:432).  Only a
+// heuristic input: k_warp never trusts it for correctness.
+__global__ void k_volume_minorant(int64_t R, int F, int field, const float2* __restrict__ vrange, double lo,
+                                  double hi, const AlphaTab tab, const RegionRec* __restrict__ rec, float* q) {
+    __shared__ double s_a[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_a[i] = tab.a[i];
+    __syncthreads();
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    const float2 v = vrange[r * F + field];
+    const double scale = 255.0 / (hi - lo);
+    double x0 = ((double)v.x - lo) * scale, x1 = ((double)v.y - lo) * scale;
+    x0 = fmin(fmax(x0, 0.0), 255.0);
+    x1 = fmin(fmax(x1, 0.0), 255.0);
+    double m = 1.0;
+    const double xs[2] = {x0, x1};
+    for (int k = 0; k < 2; k++) {
+        const int i = (int)xs[k];
+        const double f = xs[k] - (double)i;
+        const double a = i >= 255 ? s_a[255] : (1.0 - f) * s_a[i] + f * s_a[i + 1];
+        m = fmin(m, a);
+    }
+    for (int k = (int)ceil(x0); k <= (int)floor(x1); k++) m = fmin(m, s_a[k]);
+    m = fmin(fmax(m, 0.0), 0.999999);
+    const double fw = ldexp(1.0, rec[r].meta >> 24);
+    q[r] = (float)(-log1p(-m) / fw);
+}
+
 __global__ void k_volume_active(int64_t R, int F, int field, const float2* __restrict__ vrange, double lo, double hi,
                                 const AlphaTab tab, uint8_t* act) {
     __shared__ double s_a[256];
@@ -111,6 +143,9 @@ void build_active(const DevRegions& R, int kind, int field, double tf_lo, double
             AlphaTab tab;
             for (int i = 0; i < 256; i++) tab.a[i] = rgba_host[4 * i + 3];
             k_volume_active<<<grid_for(n, BS), BS, 0, s>>>(n, R.n_fields, field, R.vrange.p, tf_lo, tf_hi, tab, out.act.p);
+            out.qmin.alloc(n);
+            k_volume_minorant<<<grid_for(n, BS), BS, 0, s>>>(n, R.n_fields, field, R.vrange.p, tf_lo, tf_hi, tab,
+                                                              R.rec.p, out.qmin.p);
         } else if (kind == 1) {
             k_iso_active<<<grid_for(n, BS), BS, 0, s>>>(n, R.n_fields, field, R.vrange.p, iso, out.act.p);
         } else {

@@ -13,6 +13,7 @@ struct DevActive {
     DevBuf<uint8_t> act;     // per region
     DevBuf<uint8_t> flags;   // per k-d node
     DevBuf<uint8_t> mask4;   // per Kd4 node: active bit per child slot
+    DevBuf<float> qmin;      // volume sets: per-region opacity minorant (optical depth per unit length at spc 1)
     DevBuf<int32_t> prims;   // ascending active region ids
     double build_ms = 0.0;
 };

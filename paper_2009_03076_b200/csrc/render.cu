@@ -14,8 +14,10 @@
 // reference kernel (XB_KERNEL=tile) for A/B measurements.
 //
 // The per-pixel arithmetic is `_render_kernel` (R/render.py:521-578) in both.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <cub/cub.cuh>
 #include "march.cuh"
 #include "render.cuh"
 
@@ -383,7 +385,7 @@ __device__ __forceinline__ double sel4(int i, const double v[4]) {
 struct RaySetup {
     double d[3], inv[3];
     double rho, tmin, tmax, a, b;  // jitter, clipped range (iso-bounded), root box interval
-    int64_t out;
+    int64_t out, slot;
 };
 
 // per-ray axis data in shared memory (one copy per warp)
@@ -437,6 +439,188 @@ __device__ __forceinline__ void lattice(double ci, double co, double dt, double 
     cnt = (int)(ke - kf) + 1;
 }
 
+// ---------------------------------------------------------------------------
+// k_walk: the traversal half of the frame, one thread per ray.  Each thread
+// walks the Kd4 tree front to back with a private stack and lists the active
+// leaf regions its ray meets, in r_in order, culled only by [t_min, t_max]
+// (no restart chain, no early termination: k_warp applies both exactly while
+// it consumes the list).  A ray with more than leaf_cap leaves is marked
+// truncated and k_warp continues it with the warp frontier from the root.
+// Many small independent walks at high occupancy replace the warp frontier's
+// narrow expansion steps (a ray's k-d subtree rarely fills 32 lanes).
+
+constexpr int kWalkThreads = 128;
+constexpr int kWalkStack = 100;  // >= 3 x (Kd4 depth <= kKdStack / 2 + 1)
+constexpr int kLeafCountMask = 0x3fffffff;
+constexpr int kLeafTruncated = 0x40000000;
+
+// pixel of a ray that meets no active region: transparent, or the iso colour
+__device__ __forceinline__ void write_empty_pixel(const RenderArgs& A, int64_t slot, int64_t out, bool clip_ok) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (A.M.iso_on && clip_ok) {
+        const double f = A.iso_shade[slot];
+        if (f >= 0.0) {
+            acc[0] = A.M.iso_rgb[0] * f;
+            acc[1] = A.M.iso_rgb[1] * f;
+            acc[2] = A.M.iso_rgb[2] * f;
+            acc[3] = 1.0;
+        }
+    }
+    write_pixel(A, out, acc, 0, 0);
+}
+
+// Rays that can meet an active region (root box hit after clipping) -> flag;
+// the others get their (empty / iso-coloured) pixel here and are done.
+__global__ void __launch_bounds__(kWalkThreads) k_classify(const __grid_constant__ RenderArgs A, int64_t n_slots) {
+    const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (slot >= n_slots) return;
+    const SceneView& S = A.S;
+    const SlotPix spx = slot_pixel(A, slot);
+    bool cand = false;
+    if (spx.live) {
+        Ray r;
+        pixel_ray(A, spx.x, spx.y, r);
+        double tmin = 0.0, tmax = kTFar;
+        clip_ray(A.M, r, tmin, tmax);
+        const bool clip_ok = tmin < tmax;
+        double a = 0.0, b = -1.0;
+        slab_h(S.root_lo, S.root_hi, r, a, b);
+        cand = clip_ok && S.n_kd > 0 && a <= b && A.vflags[0];
+        if (!cand) write_empty_pixel(A, slot, spx.out, clip_ok);
+    }
+    A.leaf_count[slot] = cand ? -1 : 0;
+}
+
+// walk the candidate rays (hit_list[0, n)), one thread each; a walk lists at
+// most leaf_cap leaves (long walks are latency chains: k_warp continues those
+// rays with its parallel frontier)
+__global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ RenderArgs A, int64_t n_slots) {
+    const SceneView& S = A.S;
+    const int64_t n_cand = (int64_t)A.walk_counter[1];
+    for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < n_cand;
+         ci += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = A.hit_list[ci];
+    int count = 0, flags = 0;
+    {
+        const SlotPix spx = slot_pixel(A, slot);
+        bool clip_ok = false;
+        if (spx.live) {
+            Ray r;
+            pixel_ray(A, spx.x, spx.y, r);
+            double tmin = 0.0, tmax = kTFar;
+            clip_ray(A.M, r, tmin, tmax);
+            clip_ok = tmin < tmax;
+            if (clip_ok && A.M.iso_on) tmax = A.iso_tend[slot];
+            double a = 0.0, b = -1.0;
+            slab_h(S.root_lo, S.root_hi, r, a, b);
+            if (clip_ok && S.n_kd > 0 && a <= b && A.vflags[0]) {
+                int32_t* __restrict__ out = A.leaves + slot * (int64_t)A.leaf_cap;
+                int st_code[kWalkStack];
+                float st_tn[kWalkStack], st_tf[kWalkStack];
+                int sp_n = 0;
+                int code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
+                double tn = a, tf = b;
+                int sg[3];
+                for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
+                const float spc = (float)A.M.spc, tau_stop = A.walk_tau_stop;
+                float tau = 0.f;
+                for (;;) {
+                    if (code <= -2) {  // a leaf: list it
+                        if (count == A.leaf_cap) { flags = kLeafTruncated; break; }
+                        const int rid = -2 - code;
+                        out[count++] = rid;
+                        if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
+                            tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;
+                            if (tau > tau_stop) { flags = kLeafTruncated; break; }
+                        }
+                    } else {
+                        // expand the Kd4 node (same classification as kd_next / k_warp)
+                        const Kd4Node nd = S.kd4[code];
+                        const uint32_t msk = A.vmask4[code];
+                        int oc[4];
+                        double olo[4], ohi[4];
+                        int no = 0;
+                        int hs0 = 0, hs1 = 0, nh = 1;
+                        double hn0 = tn, hf0 = tf, hn1 = 0.0, hf1 = 0.0;
+                        {
+                            const int ax = nd.axes & 3;
+                            const double p = (double)nd.plane[0] * 0.5;
+                            const double oa = sel3(ax, r.o);
+                            const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
+                            if (sa == 0) {
+                                hs0 = oa < p ? 0 : 1;
+                            } else {
+                                const double tp = (p - oa) * sel3(ax, r.inv);
+                                const int ns_ = sa > 0 ? 0 : 1;
+                                if (tp >= tf) hs0 = ns_;
+                                else if (tp <= tn) hs0 = 1 - ns_;
+                                else { hs0 = ns_; hf0 = tp; hs1 = 1 - ns_; hn1 = tp; hf1 = tf; nh = 2; }
+                            }
+                        }
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            if (h < nh) {
+                                const int sd = h ? hs1 : hs0;
+                                const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
+                                const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
+                                int s0 = 2 * sd, s1 = -1;
+                                double a0 = hn, b0 = hf, a1 = 0.0, b1 = 0.0;
+                                if (ax != 3) {
+                                    const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
+                                    const double oa = sel3(ax, r.o);
+                                    const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
+                                    if (sa == 0) {
+                                        s0 = 2 * sd + (oa < p ? 0 : 1);
+                                    } else {
+                                        const double tp = (p - oa) * sel3(ax, r.inv);
+                                        const int nq = sa > 0 ? 0 : 1;
+                                        if (tp >= b0) s0 = 2 * sd + nq;
+                                        else if (tp <= a0) s0 = 2 * sd + 1 - nq;
+                                        else { s0 = 2 * sd + nq; b0 = tp; s1 = 2 * sd + 1 - nq; a1 = tp; b1 = hf; }
+                                    }
+                                }
+                                if (((msk >> s0) & 1) && b0 > tmin && a0 < tmax) {
+                                    oc[no] = kd4_child(nd, s0); olo[no] = a0; ohi[no] = b0; no++;
+                                }
+                                if (s1 >= 0 && ((msk >> s1) & 1) && b1 > tmin && a1 < tmax) {
+                                    oc[no] = kd4_child(nd, s1); olo[no] = a1; ohi[no] = b1; no++;
+                                }
+                            }
+                        }
+                        if (no > 0) {  // continue with the nearest child, stack the others farthest-first
+                            if (sp_n + no - 1 > kWalkStack) __trap();  // depth-bounded: <= 3 per Kd4 level
+                            for (int c = no - 1; c >= 1; c--) {
+                                st_code[sp_n] = oc[c];
+                                st_tn[sp_n] = __double2float_rd(olo[c]);
+                                st_tf[sp_n] = __double2float_ru(ohi[c]);
+                                sp_n++;
+                            }
+                            code = oc[0];
+                            tn = olo[0];
+                            tf = ohi[0];
+                            continue;
+                        }
+                    }
+                    if (sp_n == 0) break;
+                    --sp_n;
+                    code = st_code[sp_n];
+                    tn = (double)st_tn[sp_n];
+                    tf = (double)st_tf[sp_n];
+                }
+            }
+        }
+        A.leaf_count[slot] = count | flags;  // 0: k_warp writes the empty pixel
+    }
+    }
+    (void)n_slots;
+}
+
+// hit rays (leaf_count != 0) -> k_warp's work list, in slot (screen-tile) order
+struct HasLeaves {
+    const int32_t* c;
+    __device__ __forceinline__ bool operator()(const int32_t i) const { return c[i] != 0; }
+};
+
 template <int GRAD, bool ISO, bool COUNT, int MINB = kWarpMinBlocks>
 __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_constant__ RenderArgs A,
                                                                        int64_t n_slots) {
@@ -457,6 +641,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     const SceneView& S = A.S;
     const double early = A.M.early;
     unsigned long long tot_reg = 0, tot_smp = 0, tot_bytes = 0;
+    const int64_t n_work = A.leaves ? (int64_t)A.walk_counter[1] : n_slots;
 
     for (;;) {
         // ---- 32 rays per grab: every lane sets up one ray (camera ray, jitter,
@@ -465,21 +650,23 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
         //      Grab size: fixed 8 by default (C2 sweep, tools/ab.py: 32 -> 9.4 ms,
         //      16 -> 7.9, 8 -> 7.7, 4 -> 7.9, 2 -> 8.4); XB_GRAB_FIXED=0 selects a
         //      guided schedule (remaining / (grab_div x warps), clamped to [1, 32]).
+        //      With k_walk's leaf lists the work is its hit list (misses are done).
         unsigned long long b0 = 0;
         int grab = 32;
         if (lane == 0) {
             const long long seen = (long long)*(volatile unsigned long long*)A.work_counter;
-            const long long left = (long long)n_slots - seen;
+            const long long left = (long long)n_work - seen;
             const long long g = left / ((long long)A.grab_div * gridDim.x * kWarpsPerBlock);
             grab = A.grab_fixed > 0 ? A.grab_fixed : (int)max(1ll, min(32ll, g));
             b0 = atomicAdd(A.work_counter, (unsigned long long)grab);
         }
         b0 = __shfl_sync(FULL, b0, 0);
         grab = __shfl_sync(FULL, grab, 0);
-        if ((int64_t)b0 >= n_slots) break;
-        const int64_t my_slot = (int64_t)b0 + lane;
+        if ((int64_t)b0 >= n_work) break;
+        const bool my_in = lane < grab && (int64_t)b0 + lane < n_work;
+        const int64_t my_slot = A.leaves ? (my_in ? (int64_t)A.hit_list[b0 + lane] : 0) : (int64_t)b0 + lane;
         SlotPix msp = slot_pixel(A, my_slot);
-        msp.live = msp.live && lane < grab && my_slot < n_slots;
+        msp.live = msp.live && my_in;
         Ray mr;
         pixel_ray(A, msp.x, msp.y, mr);
         const double my_rho = rho_hash((uint64_t)msp.pix, A.M.seed);
@@ -489,7 +676,8 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
         if (ISO && my_clip_ok) my_tmax = A.iso_tend[my_slot];
         double my_a = 0.0, my_b = -1.0;
         slab_h(S.root_lo, S.root_hi, mr, my_a, my_b);
-        const bool my_has = my_clip_ok && S.n_kd > 0 && my_a <= my_b && A.vflags[0];
+        const int my_lraw = (A.leaves && msp.live && my_slot < n_slots) ? A.leaf_count[my_slot] : 1;
+        const bool my_has = my_clip_ok && S.n_kd > 0 && my_a <= my_b && A.vflags[0] && my_lraw != 0;
         if (msp.live && !my_has) {
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             if (ISO && my_clip_ok) {
@@ -510,6 +698,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             q.inv[0] = mr.inv[0]; q.inv[1] = mr.inv[1]; q.inv[2] = mr.inv[2];
             q.rho = my_rho; q.tmin = my_tmin; q.tmax = my_tmax; q.a = my_a; q.b = my_b;
             q.out = msp.out;
+            q.slot = my_slot;
         }
         __syncwarp();
         while (todo) {
@@ -524,7 +713,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                 r.inv[a] = q.inv[a];
             }
             const double rho = q.rho, tmin = q.tmin, tmax = q.tmax, root_a = q.a, root_b = q.b;
-            const int64_t slot = (int64_t)b0 + src;
+            const int64_t slot = q.slot;
             const int64_t out_px = q.out;
             double Tr = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;  // transmittance, premultiplied colour
             int nreg = 0, nsmp = 0;
@@ -543,13 +732,25 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                 int n = 0, spn = 0;
                 int e_code = -1;
                 double e_tn = 0.0, e_tf = 0.0;
-                n = 1;  // the root: Kd4 node 0 when the binary root is interior, else a leaf resolved at once
-                if (lane == 0) {
-                    e_code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
-                    e_tn = root_a;
-                    e_tf = root_b;
+                // leaf list of k_walk (list mode) or the frontier from the root
+                bool lmode = A.leaves != nullptr;
+                int lpos = 0, lcnt = 0;
+                bool ltrunc = false;
+                const int32_t* __restrict__ lbase = nullptr;
+                if (lmode) {
+                    const int lraw = A.leaf_count[slot];
+                    lcnt = lraw & kLeafCountMask;
+                    ltrunc = (lraw & kLeafTruncated) != 0;
+                    lbase = A.leaves + slot * (int64_t)A.leaf_cap;
+                } else {
+                    n = 1;  // the root: Kd4 node 0 when the binary root is interior, else a leaf resolved at once
+                    if (lane == 0) {
+                        e_code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
+                        e_tn = root_a;
+                        e_tf = root_b;
+                    }
                 }
-                bool walk = n > 0;
+                bool walk = true;
                 // ---- segment queue: lane i < nq holds visited region i (in ray order)
                 //      and q_P = inclusive prefix of the sample counts; h0 samples of
                 //      the queue are already composited
@@ -673,31 +874,177 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         continue;
                     }
                     if (!walk) break;
-                    // ================= traversal
-                    if (n < 32 && spn > 0) {  // refill the frontier from the spill stack (earliest on top)
-                        const int q = min(32 - n, spn);
-                        if (lane >= n && lane < n + q) {
-                            const SpillEnt f = stk[spn - 1 - (lane - n)];
-                            e_code = f.code;
-                            e_tn = (double)f.tn;
-                            e_tf = (double)f.tf;
+                    // ================= traversal: the next leaves in ray order come from
+                    //      k_walk's per-ray list (exact candidates, culled at t_min only), or,
+                    //      for a ray whose list was truncated, from the warp frontier
+                    //      restarted at the root (culled at the current t: exact as well)
+                    int take = 0, leaf_rid = 0;
+                    if (lmode) {
+                        if (lpos >= lcnt) {
+                            lmode = false;
+                            if (!ltrunc) {
+                                walk = false;
+                                continue;
+                            }
+                            n = 1;
+                            if (lane == 0) {
+                                e_code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
+                                e_tn = root_a;
+                                e_tf = root_b;
+                            }
+                            continue;
                         }
-                        spn -= q;
-                        n += q;
-                        __syncwarp();
+                        take = min(lcnt - lpos, 32 - nq);  // nq < 32 here: a full queue holds >= 32 samples
+                        if (lane < take) leaf_rid = __ldg(lbase + lpos + lane);
+                        lpos += take;
+                    } else {
+                        if (n < 32 && spn > 0) {  // refill the frontier from the spill stack (earliest on top)
+                            const int q = min(32 - n, spn);
+                            if (lane >= n && lane < n + q) {
+                                const SpillEnt f = stk[spn - 1 - (lane - n)];
+                                e_code = f.code;
+                                e_tn = (double)f.tn;
+                                e_tf = (double)f.tf;
+                            }
+                            spn -= q;
+                            n += q;
+                            __syncwarp();
+                        }
+                        if (n == 0) {
+                            walk = false;
+                            continue;
+                        }
+                        if (n == 0) {
+                            walk = false;
+                            continue;
+                        }
+                        const unsigned leafm = __ballot_sync(FULL, lane < n && e_code <= -2);
+                        const int nl = leafm == FULL ? 32 : __ffs(~leafm) - 1;
+                        if (nl == 0) {
+                            // ---- expansion step: every unresolved entry is a Kd4 node; it is
+                            //      replaced in place by its (up to 4) surviving children, near
+                            //      first.  Branch-free: each split turns the entry interval into
+                            //      the intervals of its two sides with the same exact slab
+                            //      arithmetic as kd_next (an empty side gets lo >= hi).
+                            bool actx = lane < n && e_code >= 0;
+                            if (spn + 96 > kWarpStack) {  // near the spill limit: expand the first entry only
+                                const unsigned um = __ballot_sync(FULL, actx);
+                                actx = actx && lane == __ffs(um) - 1;
+                            }
+                            int oc[4] = {e_code, 0, 0, 0};
+                            double otn[4] = {e_tn, 0.0, 0.0, 0.0}, otf[4] = {e_tf, 0.0, 0.0, 0.0};
+                            bool ov[4] = {lane < n && !actx, false, false, false};  // a resolved leaf stays in place
+                            if (actx) {
+                                const Kd4Node nd = S.kd4[e_code];
+                                const uint32_t msk = A.vmask4[e_code];
+                                // first split: one or two halves, in ray order (kd_next's classification)
+                                int hs0 = 0, hs1 = 0, nh = 1;
+                                double hn0 = e_tn, hf0 = e_tf, hn1 = 0.0, hf1 = 0.0;
+                                {
+                                    const int ax = nd.axes & 3;
+                                    const double p = (double)nd.plane[0] * 0.5;
+                                    const int sg = rs.sgn[ax];
+                                    const double oa = rs.o[ax];
+                                    if (sg == 0) {
+                                        hs0 = oa < p ? 0 : 1;
+                                    } else {
+                                        const double tp = (p - oa) * rs.inv[ax];
+                                        const int ns_ = sg > 0 ? 0 : 1;
+                                        if (tp >= e_tf) {
+                                            hs0 = ns_;
+                                        } else if (tp <= e_tn) {
+                                            hs0 = 1 - ns_;
+                                        } else {
+                                            hs0 = ns_; hf0 = tp;
+                                            hs1 = 1 - ns_; hn1 = tp; hf1 = e_tf;
+                                            nh = 2;
+                                        }
+                                    }
+                                }
+        #pragma unroll
+                                for (int h = 0; h < 2; h++) {
+                                    if (h < nh) {
+                                        const int sd = h ? hs1 : hs0;
+                                        const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
+                                        const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
+                                        int s0 = 2 * sd, s1 = -1;
+                                        double a0 = hn, bb0 = hf, a1 = 0.0, bb1 = 0.0;
+                                        if (ax != 3) {
+                                            const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
+                                            const int sg = rs.sgn[ax];
+                                            const double oa = rs.o[ax];
+                                            if (sg == 0) {
+                                                s0 = 2 * sd + (oa < p ? 0 : 1);
+                                            } else {
+                                                const double tp = (p - oa) * rs.inv[ax];
+                                                const int nqq = sg > 0 ? 0 : 1;
+                                                if (tp >= bb0) {
+                                                    s0 = 2 * sd + nqq;
+                                                } else if (tp <= a0) {
+                                                    s0 = 2 * sd + 1 - nqq;
+                                                } else {
+                                                    s0 = 2 * sd + nqq; bb0 = tp;
+                                                    s1 = 2 * sd + 1 - nqq; a1 = tp; bb1 = hf;
+                                                }
+                                            }
+                                        }
+                                        // cull: inactive subtree, or entirely before t / after tmax
+                                        ov[2 * h] = ((msk >> s0) & 1) && bb0 > t && a0 < tmax;
+                                        oc[2 * h] = kd4_child(nd, s0); otn[2 * h] = a0; otf[2 * h] = bb0;
+                                        ov[2 * h + 1] = s1 >= 0 && ((msk >> s1) & 1) && bb1 > t && a1 < tmax;
+                                        oc[2 * h + 1] = kd4_child(nd, s1 < 0 ? 0 : s1); otn[2 * h + 1] = a1; otf[2 * h + 1] = bb1;
+                                    }
+                                }
+                            }
+                            const int cnt = (int)ov[0] + (int)ov[1] + (int)ov[2] + (int)ov[3];
+                            const unsigned m1 = __ballot_sync(FULL, cnt & 1), m2 = __ballot_sync(FULL, cnt & 2),
+                                           m4 = __ballot_sync(FULL, cnt & 4);
+                            const int pos = __popc(m1 & lt_mask) + 2 * __popc(m2 & lt_mask) + 4 * __popc(m4 & lt_mask);
+                            const int total = __popc(m1) + 2 * __popc(m2) + 4 * __popc(m4);
+                            if (spn + max(0, total - 32) > kWarpStack) __trap();  // cannot happen: see the guard above
+                            int p = pos;
+        #pragma unroll
+                            for (int c = 0; c < 4; c++) {
+                                if (ov[c]) {
+                                    if (p < 32) {
+                                        s_code[wid][p] = oc[c];
+                                        s_tn[wid][p] = otn[c];
+                                        s_tfar[wid][p] = otf[c];
+                                    } else {
+                                        SpillEnt& f = stk[spn + (total - 1 - p)];
+                                        f.code = oc[c];
+                                        f.tn = __double2float_rd(otn[c]);
+                                        f.tf = __double2float_ru(otf[c]);
+                                    }
+                                    p++;
+                                }
+                            }
+                            __syncwarp();
+                            if (total > 32) spn += total - 32;
+                            n = min(total, 32);
+                            if (lane < n) {
+                                e_code = s_code[wid][lane];
+                                e_tn = s_tn[wid][lane];
+                                e_tf = s_tfar[wid][lane];
+                            }
+                            __syncwarp();
+                            continue;
+                        }
+                        take = min(nl, 32 - nq);
+                        leaf_rid = lane < take ? -2 - e_code : 0;
+                        // shift the frontier past the consumed leaves
+                        if (take < 32) {
+                            e_code = __shfl_down_sync(FULL, e_code, take);
+                            e_tn = __shfl_down_sync(FULL, e_tn, take);
+                            e_tf = __shfl_down_sync(FULL, e_tf, take);
+                        }
+                        n -= take;
                     }
-                    if (n == 0) {
-                        walk = false;
-                        continue;
-                    }
-                    const unsigned leafm = __ballot_sync(FULL, lane < n && e_code <= -2);
-                    const int nl = leafm == FULL ? 32 : __ffs(~leafm) - 1;
-                    if (nl > 0) {
+                    {
                         // ---- consume leading leaves into the segment queue: exact slab,
                         //      restart chain t_i = restart(t_out of the previous visit)
-                        const int take = min(nl, 32 - nq);  // nq < 32 here: a full queue holds >= 32 samples
                         const bool isleaf = lane < take;
-                        const int rid = isleaf ? -2 - e_code : 0;
+                        const int rid = isleaf ? leaf_rid : 0;
                         RegionRec rr{};
                         double r_in = INFINITY, r_out = -INFINITY;
                         if (isleaf) {
@@ -728,13 +1075,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             }
                             okm = __ballot_sync(FULL, ok);
                         }
-                        // shift the frontier past the consumed leaves
-                        if (take < 32) {
-                            e_code = __shfl_down_sync(FULL, e_code, take);
-                            e_tn = __shfl_down_sync(FULL, e_tn, take);
-                            e_tf = __shfl_down_sync(FULL, e_tf, take);
-                        }
-                        n -= take;
                         const int ns = __popc(okm);
                         if (stop) walk = false;
                         if (ns == 0) continue;
@@ -785,113 +1125,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         if (t >= tmax) walk = false;
                         continue;
                     }
-                    // ---- expansion step: every unresolved entry is a Kd4 node; it is
-                    //      replaced in place by its (up to 4) surviving children, near
-                    //      first.  Branch-free: each split turns the entry interval into
-                    //      the intervals of its two sides with the same exact slab
-                    //      arithmetic as kd_next (an empty side gets lo >= hi).
-                    bool actx = lane < n && e_code >= 0;
-                    if (spn + 96 > kWarpStack) {  // near the spill limit: expand the first entry only
-                        const unsigned um = __ballot_sync(FULL, actx);
-                        actx = actx && lane == __ffs(um) - 1;
-                    }
-                    int oc[4] = {e_code, 0, 0, 0};
-                    double otn[4] = {e_tn, 0.0, 0.0, 0.0}, otf[4] = {e_tf, 0.0, 0.0, 0.0};
-                    bool ov[4] = {lane < n && !actx, false, false, false};  // a resolved leaf stays in place
-                    if (actx) {
-                        const Kd4Node nd = S.kd4[e_code];
-                        const uint32_t msk = A.vmask4[e_code];
-                        // first split: one or two halves, in ray order (kd_next's classification)
-                        int hs0 = 0, hs1 = 0, nh = 1;
-                        double hn0 = e_tn, hf0 = e_tf, hn1 = 0.0, hf1 = 0.0;
-                        {
-                            const int ax = nd.axes & 3;
-                            const double p = (double)nd.plane[0] * 0.5;
-                            const int sg = rs.sgn[ax];
-                            const double oa = rs.o[ax];
-                            if (sg == 0) {
-                                hs0 = oa < p ? 0 : 1;
-                            } else {
-                                const double tp = (p - oa) * rs.inv[ax];
-                                const int ns_ = sg > 0 ? 0 : 1;
-                                if (tp >= e_tf) {
-                                    hs0 = ns_;
-                                } else if (tp <= e_tn) {
-                                    hs0 = 1 - ns_;
-                                } else {
-                                    hs0 = ns_; hf0 = tp;
-                                    hs1 = 1 - ns_; hn1 = tp; hf1 = e_tf;
-                                    nh = 2;
-                                }
-                            }
-                        }
-#pragma unroll
-                        for (int h = 0; h < 2; h++) {
-                            if (h < nh) {
-                                const int sd = h ? hs1 : hs0;
-                                const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
-                                const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
-                                int s0 = 2 * sd, s1 = -1;
-                                double a0 = hn, bb0 = hf, a1 = 0.0, bb1 = 0.0;
-                                if (ax != 3) {
-                                    const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
-                                    const int sg = rs.sgn[ax];
-                                    const double oa = rs.o[ax];
-                                    if (sg == 0) {
-                                        s0 = 2 * sd + (oa < p ? 0 : 1);
-                                    } else {
-                                        const double tp = (p - oa) * rs.inv[ax];
-                                        const int nqq = sg > 0 ? 0 : 1;
-                                        if (tp >= bb0) {
-                                            s0 = 2 * sd + nqq;
-                                        } else if (tp <= a0) {
-                                            s0 = 2 * sd + 1 - nqq;
-                                        } else {
-                                            s0 = 2 * sd + nqq; bb0 = tp;
-                                            s1 = 2 * sd + 1 - nqq; a1 = tp; bb1 = hf;
-                                        }
-                                    }
-                                }
-                                // cull: inactive subtree, or entirely before t / after tmax
-                                ov[2 * h] = ((msk >> s0) & 1) && bb0 > t && a0 < tmax;
-                                oc[2 * h] = kd4_child(nd, s0); otn[2 * h] = a0; otf[2 * h] = bb0;
-                                ov[2 * h + 1] = s1 >= 0 && ((msk >> s1) & 1) && bb1 > t && a1 < tmax;
-                                oc[2 * h + 1] = kd4_child(nd, s1 < 0 ? 0 : s1); otn[2 * h + 1] = a1; otf[2 * h + 1] = bb1;
-                            }
-                        }
-                    }
-                    const int cnt = (int)ov[0] + (int)ov[1] + (int)ov[2] + (int)ov[3];
-                    const unsigned m1 = __ballot_sync(FULL, cnt & 1), m2 = __ballot_sync(FULL, cnt & 2),
-                                   m4 = __ballot_sync(FULL, cnt & 4);
-                    const int pos = __popc(m1 & lt_mask) + 2 * __popc(m2 & lt_mask) + 4 * __popc(m4 & lt_mask);
-                    const int total = __popc(m1) + 2 * __popc(m2) + 4 * __popc(m4);
-                    if (spn + max(0, total - 32) > kWarpStack) __trap();  // cannot happen: see the guard above
-                    int p = pos;
-#pragma unroll
-                    for (int c = 0; c < 4; c++) {
-                        if (ov[c]) {
-                            if (p < 32) {
-                                s_code[wid][p] = oc[c];
-                                s_tn[wid][p] = otn[c];
-                                s_tfar[wid][p] = otf[c];
-                            } else {
-                                SpillEnt& f = stk[spn + (total - 1 - p)];
-                                f.code = oc[c];
-                                f.tn = __double2float_rd(otn[c]);
-                                f.tf = __double2float_ru(otf[c]);
-                            }
-                            p++;
-                        }
-                    }
-                    __syncwarp();
-                    if (total > 32) spn += total - 32;
-                    n = min(total, 32);
-                    if (lane < n) {
-                        e_code = s_code[wid][lane];
-                        e_tn = s_tn[wid][lane];
-                        e_tf = s_tfar[wid][lane];
-                    }
-                    __syncwarp();
                 }
             }
             if (lane == 0) {
@@ -1044,6 +1277,27 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         }
     } else {
         threads = kWarpThreads;
+        if (A.leaves) {
+            RenderArgs& W = const_cast<RenderArgs&>(A);
+            const double e = std::min(A.M.early, 0.999999);
+            W.walk_tau_stop = (float)(-std::log(1.0 - e) + 2.0);  // opacity >= 1 - e^-tau, with margin
+            if (getenv("XB_WALK_NOTAU")) W.walk_tau_stop = INFINITY;
+            void* wargs[] = {(void*)&A, (void*)&n_slots};
+            XB_CUDA(cudaLaunchKernel((const void*)k_classify, dim3(grid_for(n_slots, kWalkThreads)),
+                                     dim3(kWalkThreads), wargs, 0, s));
+            size_t tb = 0;
+            cub::CountingInputIterator<int32_t> it(0);
+            XB_CUDA(cub::DeviceSelect::If(nullptr, tb, it, A.hit_list, A.walk_counter + 1, (int)n_slots,
+                                          HasLeaves{A.leaf_count}, s));
+            void* tmp = nullptr;
+            XB_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 16), s));
+            XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.hit_list, A.walk_counter + 1, (int)n_slots,
+                                          HasLeaves{A.leaf_count}, s));
+            // one thread per candidate (blocks past the device-side count exit at once)
+            XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
+                                     wargs, 0, s));
+            XB_CUDA(cudaFreeAsync(tmp, s));
+        }
         if (g == 0) fn = iso ? warp_fn<0, true>(count) : warp_fn<0, false>(count);
         else if (g == 1) fn = iso ? warp_fn<1, true>(count) : warp_fn<1, false>(count);
         else fn = iso ? warp_fn<2, true>(count) : warp_fn<2, false>(count);

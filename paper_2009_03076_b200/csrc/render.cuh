@@ -27,6 +27,13 @@ struct RenderArgs {
     unsigned long long* stats;  // [regions, samples, algorithmic bytes]
     unsigned long long* work_counter;  // k_frame / k_warp slot counter (zeroed per launch)
     int grab_div, grab_fixed;          // k_warp grab schedule (launch_render)
+    int32_t* leaves;                   // k_walk -> k_warp: per slot leaf_cap region ids in ray order (or NULL)
+    int32_t* leaf_count;               // per slot: count | 0x40000000 when truncated
+    int leaf_cap;
+    const float* vqmin;                // per region opacity minorant (k_walk early stop), may be NULL
+    unsigned long long* walk_counter;  // k_walk slot counter, then the hit-list length
+    int32_t* hit_list;                 // slots k_walk found to meet an active region (k_warp's work)
+    float walk_tau_stop;               // k_walk stops listing once the opacity minorant passes this depth
     double* iso_tend;           // per slot: volume t_end (iso hit or clip end)
     double* iso_shade;          // per slot: headlight factor of the iso hit, < 0 when none
     double tf[1024];

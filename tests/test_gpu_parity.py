@@ -200,21 +200,31 @@ def _params(meta):
                        seed=meta["seed"], gradient_mode=meta["gradient_mode"], clip_planes=planes)
 
 
+KERNEL_ENVS = {
+    "warp": {},                        # default: k_classify + k_walk leaf lists + k_warp
+    "warp_cap1": {"XB_LEAF_CAP": "1"},  # every long ray falls back to the warp frontier
+    "warp_nowalk": {"XB_WALK": "0"},   # k_warp's frontier only
+    "frame": {"XB_KERNEL": "frame"},   # per-lane persistent kernel
+    "tile": {"XB_KERNEL": "tile"},     # one thread per pixel
+}
+_ENV_KEYS = ("XB_KERNEL", "XB_LEAF_CAP", "XB_WALK")
+
+
 @pytest.fixture
 def kernel_env(request):
-    """XB_KERNEL selects the march kernel: warp (default), frame (per-lane persistent), tile."""
+    """Select the march-kernel variant through its environment switches."""
     import os
 
-    old = os.environ.pop("XB_KERNEL", None)
-    if request.param != "warp":
-        os.environ["XB_KERNEL"] = request.param
+    old = {k: os.environ.pop(k, None) for k in _ENV_KEYS}
+    os.environ.update(KERNEL_ENVS[request.param])
     yield request.param
-    os.environ.pop("XB_KERNEL", None)
-    if old is not None:
-        os.environ["XB_KERNEL"] = old
+    for k in _ENV_KEYS:
+        os.environ.pop(k, None)
+        if old[k] is not None:
+            os.environ[k] = old[k]
 
 
-@pytest.mark.parametrize("kernel_env", ["warp", "frame", "tile"], indirect=True)
+@pytest.mark.parametrize("kernel_env", sorted(KERNEL_ENVS), indirect=True)
 @pytest.mark.parametrize("key", _frame_keys())
 def test_frames_match_reference(xb, key, frames, kernel_env):
     from paper_2009_03076_b200.accel import TransferFunction
@@ -374,12 +384,13 @@ def test_acceptance_million_cells_vs_oracle(xb):
     # repetition
     import os
 
-    for kern in ("tile", "frame"):
-        os.environ["XB_KERNEL"] = kern
+    for kern in ("tile", "frame", "warp_cap1", "warp_nowalk"):
+        os.environ.update(KERNEL_ENVS[kern])
         try:
             u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)
         finally:
-            del os.environ["XB_KERNEL"]
+            for k in _ENV_KEYS:
+                os.environ.pop(k, None)
         assert np.array_equal(cnt, cntt), kern
         assert np.abs(f64 - f64t).max() <= RGBA_TOL, kern
     for _ in range(3):

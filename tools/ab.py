@@ -30,9 +30,15 @@ stream = torch.cuda.current_stream()
 
 def setv(v):
     """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N) | gD (guided grab divisor D)"""
-    for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED"):
+    for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU"):
         os.environ.pop(k, None)
-    if v.startswith("f") and v[1:].isdigit():
+    if v == "notau":
+        os.environ["XB_WALK_NOTAU"] = "1"
+    elif v == "nowalk":
+        os.environ["XB_WALK"] = "0"
+    elif v.startswith("cap") and v[3:].isdigit():
+        os.environ["XB_LEAF_CAP"] = v[3:]
+    elif v.startswith("f") and v[1:].isdigit():
         os.environ["XB_GRAB_FIXED"] = v[1:]
     elif v.startswith("g") and v[1:].isdigit():
         os.environ["XB_GRAB_DIV"] = v[1:]

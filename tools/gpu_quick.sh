@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench_def.json 2> gpurun_out/bench_def.err; tail -c 2500 gpurun_out/bench_def.json; tail -3 gpurun_out/bench_def.err
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -c 1500 gpurun_out/bench_ref.json; tail -3 gpurun_out/bench_ref.err
+timeout 1200 python -m pytest tests -q -m gpu -x --timeout 900 > gpurun_out/pt_walk6.log 2>&1; tail -1 gpurun_out/pt_walk6.log
+timeout 300 python tools/ab.py c2 warp,nowalk 6 > gpurun_out/ab_walk6.log 2>&1; grep median gpurun_out/ab_walk6.log
+timeout 300 python tools/ab.py c3 warp,nowalk 6 > gpurun_out/ab_walk6c3.log 2>&1; grep median gpurun_out/ab_walk6c3.log
