@@ -168,6 +168,22 @@ int xb_trace_intervals(const xb_model* m, const xb_regions* r, const xb_active* 
                        const double* d, double t_start, double t_max, int32_t cap, double* t_in, double* t_out,
                        int32_t* region, int32_t* count);
 
+/* ---- LBVH over an active set: RegionBvh (R/accel.py:125-224), _bvh_next_hit / _bvh_point_query (285-388) ----
+ * Morton-sorted, Karras-built, refit on the GPU on first use.  Node arrays in
+ * the reference's RegionBvh layout: 2n-1 nodes (internal, then one leaf per
+ * region), f64 boxes (n,3), left/right (-1 at leaves), start (i64) / count
+ * into prims; an empty set gives the reference's single dummy node. */
+int xb_active_lbvh_info(const xb_active* a, int64_t* n_nodes, int32_t* depth, double* build_ms);
+int xb_active_lbvh_download(const xb_active* a, double* node_lo, double* node_hi, int32_t* left, int32_t* right,
+                            int64_t* start, int32_t* count, int32_t* prims);
+/* iterate_intervals with one LBVH closest-hit query per region (the reference's traversal) */
+int xb_trace_intervals_lbvh(const xb_model* m, const xb_regions* r, const xb_active* a, int64_t n, const double* o,
+                            const double* d, double t_start, double t_max, int32_t cap, double* t_in, double* t_out,
+                            int32_t* region, int32_t* count);
+/* point_query (R/accel.py:408-411): active region whose half-open box holds p, else -1 */
+int xb_point_query_lbvh(const xb_model* m, const xb_regions* r, const xb_active* a, int64_t n, const double* p,
+                        int32_t* region);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

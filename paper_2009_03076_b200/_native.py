@@ -86,6 +86,10 @@ SIGNATURES = {
     "xb_sample_points": (C.c_int, [P, P, i32, i64, P, P, i32, P, P]),
     "xb_sample_scan": (C.c_int, [P, i32, i64, P, P]),
     "xb_trace_intervals": (C.c_int, [P, P, P, i64, P, P, f64, f64, i32, P, P, P, P]),
+    "xb_active_lbvh_info": (C.c_int, [P, P, P, P]),
+    "xb_active_lbvh_download": (C.c_int, [P, P, P, P, P, P, P, P]),
+    "xb_trace_intervals_lbvh": (C.c_int, [P, P, P, i64, P, P, f64, f64, i32, P, P, P, P]),
+    "xb_point_query_lbvh": (C.c_int, [P, P, P, i64, P, P]),
 }
 
 _lock = threading.Lock()

@@ -115,7 +115,12 @@ class RayInterval:
 
 class RegionBvh:
     """Active region set on the GPU — the B200 form of the reference's RegionBvh
-    (R/accel.py:125-155): a per-region active flag + per-k-d-node subtree flags.
+    (R/accel.py:125-155): a per-region active flag + per-k-d-node subtree flags
+    for the frame kernel, and an LBVH (Morton sort + Karras build, csrc/lbvh.cu)
+    whose node arrays carry the reference's names (`node_lo`, `node_hi`,
+    `node_left`, `node_right`, `node_start`, `node_count`, `leaf_prims`,
+    `kernel_args()`); topology differs from the reference's median split, which
+    the queries' results do not depend on.
 
     `prims` lists the active region ids (ascending); `build_ms` is the device
     build time (reported as `bvhRebuildMs` on edits, R/render.py:119-132).
@@ -152,6 +157,36 @@ class RegionBvh:
             N.check(N.lib().xb_active_prims(self._h.h, N.ptr(p)))
             self._prims = p
         return self._prims
+
+    def _lbvh(self):
+        if getattr(self, "_nodes", None) is None:
+            L = N.lib()
+            nn, depth, ms = C.c_int64(), C.c_int32(), C.c_double()
+            N.check(L.xb_active_lbvh_info(self._h.h, C.byref(nn), C.byref(depth), C.byref(ms)))
+            n = nn.value
+            lo, hi = np.empty((n, 3)), np.empty((n, 3))
+            left, right = np.empty(n, np.int32), np.empty(n, np.int32)
+            start, count = np.empty(n, np.int64), np.empty(n, np.int32)
+            prims = np.empty(max(self._n_active, 1), np.int32)
+            N.check(L.xb_active_lbvh_download(self._h.h, N.ptr(lo), N.ptr(hi), N.ptr(left), N.ptr(right),
+                                              N.ptr(start), N.ptr(count), N.ptr(prims)))
+            self._nodes = (lo, hi, left, right, start, count, prims[: self._n_active])
+            self.lbvh_depth = depth.value
+            self.lbvh_build_ms = ms.value
+        return self._nodes
+
+    node_lo = property(lambda self: self._lbvh()[0])
+    node_hi = property(lambda self: self._lbvh()[1])
+    node_left = property(lambda self: self._lbvh()[2])
+    node_right = property(lambda self: self._lbvh()[3])
+    node_start = property(lambda self: self._lbvh()[4])
+    node_count = property(lambda self: self._lbvh()[5])
+    leaf_prims = property(lambda self: self._lbvh()[6])
+
+    def kernel_args(self):
+        """The reference's argument tuple (R/accel.py:150-155), LBVH leaf order."""
+        lo, hi, left, right, start, count, prims = self._lbvh()
+        return lo, hi, left, right, start, count, prims, self.regions.lo, self.regions.hi
 
     @property
     def active_mask(self) -> np.ndarray:
@@ -200,8 +235,14 @@ def restart_epsilon(t_out: float) -> float:
     return max(1e-7, 1e-7 * t_out)
 
 
-def trace_rays(bvh: RegionBvh, origins, directions, t_start: float, t_max: float, cap: int = 256):
-    """Batch `iterate_intervals` on the GPU: list of [(t_in, t_out, region), ...] per ray."""
+def trace_rays(bvh: RegionBvh, origins, directions, t_start: float, t_max: float, cap: int = 256,
+               traversal: str = "kd"):
+    """Batch `iterate_intervals` on the GPU: list of [(t_in, t_out, region), ...] per ray.
+
+    traversal "kd": the ordered k-d walk (one walk per ray); "lbvh": one LBVH
+    closest-hit query per region visit, the reference's own scheme."""
+    if traversal not in ("kd", "lbvh"):
+        raise ValueError(f"unknown traversal {traversal!r}")
     o = np.ascontiguousarray(np.asarray(origins, np.float64).reshape(-1, 3))
     d = np.ascontiguousarray(np.asarray(directions, np.float64).reshape(-1, 3))
     n = len(o)
@@ -211,8 +252,9 @@ def trace_rays(bvh: RegionBvh, origins, directions, t_start: float, t_max: float
         tin, tout = np.empty((n, cap)), np.empty((n, cap))
         reg = np.empty((n, cap), np.int32)
         cnt = np.empty(n, np.int32)
-        N.check(L.xb_trace_intervals(rh.model_handle.h, rh.h, bvh.handle.h, n, N.ptr(o), N.ptr(d), float(t_start),
-                                     float(t_max), cap, N.ptr(tin), N.ptr(tout), N.ptr(reg), N.ptr(cnt)))
+        fn = L.xb_trace_intervals if traversal == "kd" else L.xb_trace_intervals_lbvh
+        N.check(fn(rh.model_handle.h, rh.h, bvh.handle.h, n, N.ptr(o), N.ptr(d), float(t_start), float(t_max), cap,
+                   N.ptr(tin), N.ptr(tout), N.ptr(reg), N.ptr(cnt)))
         if n == 0 or cnt.max() <= cap:
             break
         cap = int(cnt.max())
@@ -220,21 +262,27 @@ def trace_rays(bvh: RegionBvh, origins, directions, t_start: float, t_max: float
 
 
 def next_region(bvh: RegionBvh, origin, direction, t_start: float, t_max: float) -> Optional[RayInterval]:
-    """Closest active region with entry >= t_start, clipped to [t_start, t_max] (R/accel.py:396-405)."""
-    got = trace_rays(bvh, origin, direction, t_start, t_max, cap=1)[0]
+    """Closest active region with entry >= t_start, clipped to [t_start, t_max] (R/accel.py:396-405):
+    one LBVH closest-hit query."""
+    got = trace_rays(bvh, origin, direction, t_start, t_max, cap=1, traversal="lbvh")[0]
     if not got:
         return None
     return RayInterval(*got[0])
 
 
 def point_query(bvh: RegionBvh, p) -> Optional[int]:
-    """Active region whose half-open box contains p (R/accel.py:408-411)."""
-    from .sampling import locate_points
+    """Active region whose half-open box contains p (R/accel.py:408-411): LBVH point query."""
+    r = int(point_query_batch(bvh, np.asarray(p, np.float64).reshape(1, 3))[0])
+    return None if r < 0 else r
 
-    r = int(locate_points(bvh.regions, np.asarray(p, np.float64).reshape(1, 3))[0])
-    if r < 0 or not bvh.active_mask[r]:
-        return None
-    return r
+
+def point_query_batch(bvh: RegionBvh, points) -> np.ndarray:
+    """`point_query` for (n, 3) points on the GPU; -1 where no active region holds the point."""
+    p = np.ascontiguousarray(np.asarray(points, np.float64).reshape(-1, 3))
+    out = np.empty(len(p), np.int32)
+    rh = bvh.handle.regions_handle
+    N.check(N.lib().xb_point_query_lbvh(rh.model_handle.h, rh.h, bvh.handle.h, len(p), N.ptr(p), N.ptr(out)))
+    return out
 
 
 def iterate_intervals(bvh: RegionBvh, origin, direction, t_start: float, t_max: float):

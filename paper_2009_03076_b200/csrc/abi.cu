@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <vector>
 #include "../../include/exabricks.h"
 #include "accel.cuh"
 #include "render.cuh"
@@ -467,6 +468,15 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         check_active(vol, r, "volume");
         A->vflags = vol->a.flags.p;
         A->vmask4 = vol->a.mask4.p;
+        A->use_lbvh = 0;
+        {
+            const char* tr = getenv("XB_TRAVERSAL");
+            if (tr && strcmp(tr, "lbvh") == 0) {
+                A->use_lbvh = 1;
+                A->vlb = xb::active_lbvh(r->r, vol->a, s).view();
+                A->ilb = (mp->iso_on && iso) ? xb::active_lbvh(r->r, iso->a, s).view() : A->vlb;
+            }
+        }
         A->vqmin = vol->a.qmin.n ? vol->a.qmin.p : nullptr;
         fill_march(A->M, mp);
         A->M.iso_on = (mp->iso_on && iso) ? 1 : 0;
@@ -581,6 +591,14 @@ static int run_rays(const xb_model* m, const xb_regions* r, int32_t field, const
         B->iflags = act->a.flags.p;
         fill_march(B->M, mp);
         B->mode = mode;
+        B->use_lbvh = 0;
+        {
+            const char* tr = getenv("XB_TRAVERSAL");
+            if (tr && strcmp(tr, "lbvh") == 0) {
+                B->use_lbvh = 1;
+                B->vlb = B->ilb = xb::active_lbvh(r->r, act->a, st.s).view();
+            }
+        }
         B->n = n;
         std::memcpy(B->tf, mp->tf_rgba, sizeof(B->tf));
         xb::DevBuf<double> dO, dD, d0, d1, dr, dout;
@@ -677,6 +695,117 @@ int xb_trace_intervals(const xb_model* m, const xb_regions* r, const xb_active* 
         dq.download(t_out, (size_t)n * cap, st.s);
         dr.download(region, (size_t)n * cap, st.s);
         dc.download(count, n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+// ---- LBVH (RegionBvh node arrays, closest-hit / point queries) ----
+
+int xb_active_lbvh_info(const xb_active* a, int64_t* n_nodes, int32_t* depth, double* build_ms) {
+    return guarded([&] {
+        XB_CHECK(a != nullptr && a->owner != nullptr, XB_ERR_ARG, "null active set");
+        xb::DeviceGuard g(a->a.device);
+        OwnedStream st;
+        const xb::DevLbvh& L = xb::active_lbvh(a->owner->r, a->a, st.s);
+        if (n_nodes) *n_nodes = L.n_prims ? 2 * L.n_prims - 1 : 1;
+        if (depth) *depth = L.depth;
+        if (build_ms) *build_ms = L.build_ms;
+    });
+}
+
+int xb_active_lbvh_download(const xb_active* a, double* node_lo, double* node_hi, int32_t* left, int32_t* right,
+                            int64_t* start, int32_t* count, int32_t* prims) {
+    return guarded([&] {
+        XB_CHECK(a != nullptr && a->owner != nullptr, XB_ERR_ARG, "null active set");
+        xb::DeviceGuard g(a->a.device);
+        OwnedStream st;
+        const xb::DevLbvh& L = xb::active_lbvh(a->owner->r, a->a, st.s);
+        const int64_t n = L.n_prims;
+        if (n == 0) {  // the reference's dummy node (R/accel.py:205-212)
+            for (int c = 0; c < 3; c++) {
+                node_lo[c] = INFINITY;
+                node_hi[c] = -INFINITY;
+            }
+            left[0] = right[0] = -1;
+            start[0] = 0;
+            count[0] = 0;
+            return;
+        }
+        std::vector<xb::LbvhNode> nodes(std::max<int64_t>(n - 1, 0));
+        std::vector<xb::RegionRec> rec(a->owner->r.n_regions);
+        std::vector<int32_t> pr(n);
+        if (n > 1) L.nodes.download(nodes.data(), n - 1, st.s);
+        L.prims.download(pr.data(), n, st.s);
+        a->owner->r.rec.download(rec.data(), rec.size(), st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+        // internal node i -> i, leaf k -> (n - 1) + k; leaves hold one region (start k, count 1)
+        auto node_of = [&](int32_t c) -> int64_t { return c >= 0 ? c : (n - 1) + (int64_t)(~c); };
+        for (int64_t i = 0; i < n - 1; i++) {
+            for (int c = 0; c < 3; c++) {
+                node_lo[3 * i + c] = nodes[i].lo[c] * 0.5;
+                node_hi[3 * i + c] = nodes[i].hi[c] * 0.5;
+            }
+            left[i] = (int32_t)node_of(nodes[i].left);
+            right[i] = (int32_t)node_of(nodes[i].right);
+            start[i] = 0;
+            count[i] = 0;
+        }
+        for (int64_t k = 0; k < n; k++) {
+            const int64_t i = n - 1 + k;
+            const xb::RegionRec& rr = rec[pr[k]];
+            for (int c = 0; c < 3; c++) {
+                node_lo[3 * i + c] = rr.lo[c] * 0.5;
+                node_hi[3 * i + c] = rr.hi[c] * 0.5;
+            }
+            left[i] = right[i] = -1;
+            start[i] = k;
+            count[i] = 1;
+            prims[k] = pr[k];
+        }
+    });
+}
+
+int xb_trace_intervals_lbvh(const xb_model* m, const xb_regions* r, const xb_active* a, int64_t n, const double* o,
+                            const double* d, double t_start, double t_max, int32_t cap, double* t_in, double* t_out,
+                            int32_t* region, int32_t* count) {
+    return guarded([&] {
+        XB_CHECK(n >= 0 && cap >= 0, XB_ERR_ARG, "bad trace arguments");
+        xb::DeviceGuard g(m->m.device);
+        OwnedStream st;
+        const xb::SceneView S = scene_view(m, r, 0);
+        check_active(a, r, "trace");
+        const xb::LbvhView L = xb::active_lbvh(r->r, a->a, st.s).view();
+        xb::DevBuf<double> dO, dD, di, dq;
+        xb::DevBuf<int32_t> dr, dc;
+        dO.upload(o, 3 * n, st.s);
+        dD.upload(d, 3 * n, st.s);
+        di.alloc((size_t)n * cap + 1);
+        dq.alloc((size_t)n * cap + 1);
+        dr.alloc((size_t)n * cap + 1);
+        dc.alloc(n + 1);
+        xb::trace_intervals(S, a->a.flags.p, n, dO.p, dD.p, t_start, t_max, cap, di.p, dq.p, dr.p, dc.p, st.s, &L);
+        di.download(t_in, (size_t)n * cap, st.s);
+        dq.download(t_out, (size_t)n * cap, st.s);
+        dr.download(region, (size_t)n * cap, st.s);
+        dc.download(count, n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int xb_point_query_lbvh(const xb_model* m, const xb_regions* r, const xb_active* a, int64_t n, const double* p,
+                        int32_t* region) {
+    return guarded([&] {
+        XB_CHECK(n >= 0, XB_ERR_ARG, "bad point count");
+        xb::DeviceGuard g(m->m.device);
+        OwnedStream st;
+        const xb::SceneView S = scene_view(m, r, 0);
+        check_active(a, r, "point query");
+        const xb::LbvhView L = xb::active_lbvh(r->r, a->a, st.s).view();
+        xb::DevBuf<double> dp;
+        xb::DevBuf<int32_t> dr(n + 1);
+        dp.upload(p, 3 * n, st.s);
+        xb::point_query_lbvh(S, L, n, dp.p, dr.p, st.s);
+        dr.download(region, n, st.s);
         XB_CUDA(cudaStreamSynchronize(st.s));
     });
 }

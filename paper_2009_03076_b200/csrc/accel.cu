@@ -261,7 +261,7 @@ __global__ void k_sample_scan(SceneView S, int64_t n_bricks, int64_t n, const do
 // k-d walk; up to `cap` intervals per ray.
 __global__ void k_trace(SceneView S, const uint8_t* __restrict__ flags, int64_t n, const double* __restrict__ o,
                         const double* __restrict__ d, double t_start, double t_max, int cap, double* tin, double* tout,
-                        int32_t* reg, int32_t* cnt) {
+                        int32_t* reg, int32_t* cnt, LbvhView L, int use_lb) {
     const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= n) return;
     Ray r;
@@ -277,7 +277,9 @@ __global__ void k_trace(SceneView S, const uint8_t* __restrict__ flags, int64_t 
     for (;;) {
         int rid;
         double ci, co;
-        if (!kd_next(S, flags, r, w, t, t_max, rid, ci, co)) break;
+        // ordered k-d walk, or the reference's per-visit closest-hit query on the LBVH
+        if (!(use_lb ? lbvh_next_hit(S, L, r, t, t_max, rid, ci, co) : kd_next(S, flags, r, w, t, t_max, rid, ci, co)))
+            break;
         if (k < cap) {
             tin[q * cap + k] = ci;
             tout[q * cap + k] = co;
@@ -312,10 +314,36 @@ void sample_scan(const SceneView& S, int64_t n_bricks, int64_t n, const double* 
 }
 
 void trace_intervals(const SceneView& S, const uint8_t* flags, int64_t n, const double* o, const double* d, double t0,
-                     double t1, int cap, double* tin, double* tout, int32_t* reg, int32_t* cnt, cudaStream_t s) {
+                     double t1, int cap, double* tin, double* tout, int32_t* reg, int32_t* cnt, cudaStream_t s,
+                     const LbvhView* lb) {
     if (n <= 0) return;
-    k_trace<<<grid_for(n, 64), 64, 0, s>>>(S, flags, n, o, d, t0, t1, cap, tin, tout, reg, cnt);
+    const LbvhView L = lb ? *lb : LbvhView{nullptr, nullptr, 0};
+    k_trace<<<grid_for(n, 64), 64, 0, s>>>(S, flags, n, o, d, t0, t1, cap, tin, tout, reg, cnt, L, lb ? 1 : 0);
     check_launch("k_trace");
+}
+
+namespace {
+__global__ void k_point_lbvh(SceneView S, LbvhView L, int64_t n, const double* __restrict__ p, int32_t* out) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < n) out[q] = lbvh_point(S, L, p[3 * q], p[3 * q + 1], p[3 * q + 2]);
+}
+}  // namespace
+
+void point_query_lbvh(const SceneView& S, const LbvhView& L, int64_t n, const double* p, int32_t* out, cudaStream_t s) {
+    if (n <= 0) return;
+    k_point_lbvh<<<grid_for(n, 64), 64, 0, s>>>(S, L, n, p, out);
+    check_launch("k_point_lbvh");
+}
+
+const DevLbvh& active_lbvh(const DevRegions& R, const DevActive& a, cudaStream_t s) {
+    std::lock_guard<std::mutex> g(a.lb_mu);
+    if (!a.lb) {
+        auto lb = std::make_unique<DevLbvh>();
+        build_lbvh(R, a.prims.p, a.n_active, *lb, s);
+        XB_CUDA(cudaStreamSynchronize(s));
+        a.lb = std::move(lb);
+    }
+    return *a.lb;
 }
 
 }  // namespace xb

@@ -1,6 +1,8 @@
 // accel.cuh — active sets and point / interval queries.
 #pragma once
-#include "march.cuh"
+#include <memory>
+#include <mutex>
+#include "lbvh.cuh"
 
 namespace xb {
 
@@ -16,7 +18,12 @@ struct DevActive {
     DevBuf<float> qmin;      // volume sets: per-region opacity minorant (optical depth per unit length at spc 1)
     DevBuf<int32_t> prims;   // ascending active region ids
     double build_ms = 0.0;
+    // LBVH over the active regions (RegionBvh node arrays / closest-hit queries), built on first use
+    mutable std::mutex lb_mu;
+    mutable std::unique_ptr<DevLbvh> lb;
 };
+
+const DevLbvh& active_lbvh(const DevRegions& R, const DevActive& a, cudaStream_t s);
 
 void build_kd4(DevRegions& R, cudaStream_t s);
 void build_kd4_mask(const DevRegions& R, const uint8_t* flags, DevBuf<uint8_t>& mask, cudaStream_t s);
@@ -28,6 +35,8 @@ void sample_points(const SceneView& S, int64_t n, const double* p, const int32_t
                    double* out, cudaStream_t s);
 void sample_scan(const SceneView& S, int64_t n_bricks, int64_t n, const double* p, double* out, cudaStream_t s);
 void trace_intervals(const SceneView& S, const uint8_t* flags, int64_t n, const double* o, const double* d, double t0,
-                     double t1, int cap, double* tin, double* tout, int32_t* reg, int32_t* cnt, cudaStream_t s);
+                     double t1, int cap, double* tin, double* tout, int32_t* reg, int32_t* cnt, cudaStream_t s,
+                     const LbvhView* lb = nullptr);
+void point_query_lbvh(const SceneView& S, const LbvhView& L, int64_t n, const double* p, int32_t* out, cudaStream_t s);
 
 }  // namespace xb

@@ -255,6 +255,115 @@ __device__ __forceinline__ int kd_point(const SceneView& S, double px, double py
 }
 
 // ---------------------------------------------------------------------------
+// LBVH traversal (csrc/lbvh.cu builds the tree; see lbvh.cuh)
+
+struct __align__(16) LbvhNode {
+    int32_t lo[3], hi[3];  // half-unit box (exact: union of region boxes)
+    int32_t left, right;   // >= 0: internal node; < 0: leaf ~k -> prims[k]
+};
+static_assert(sizeof(LbvhNode) == 32, "LbvhNode is 32 bytes");
+
+constexpr int kLbvhStack = 128;  // R/accel.py:297 uses the same depth
+
+struct LbvhView {
+    const LbvhNode* __restrict__ nodes;  // n_prims - 1 internal nodes, root 0
+    const int32_t* __restrict__ prims;   // active region ids in Morton order
+    int64_t n_prims;
+};
+
+// box of a child reference (internal node or leaf region)
+__device__ __forceinline__ void lbvh_child_box(const SceneView& S, const LbvhView& L, int32_t c, const int32_t*& lo,
+                                               const int32_t*& hi) {
+    if (c >= 0) {
+        lo = L.nodes[c].lo;
+        hi = L.nodes[c].hi;
+    } else {
+        const RegionRec& rr = S.rec[L.prims[~c]];
+        lo = rr.lo;
+        hi = rr.hi;
+    }
+}
+
+// _bvh_next_hit (R/accel.py:285-352): closest active region with clipped entry
+// max(r_in, t) < min(r_out, t_max); ties -> lower region id.
+__device__ inline bool lbvh_next_hit(const SceneView& S, const LbvhView& L, const Ray& r, double t_start,
+                                     double t_max, int& rid, double& c_in_o, double& c_out_o) {
+    int best_r = -1;
+    double best_in = INFINITY, best_out = INFINITY;
+    if (L.n_prims == 0) return false;
+    int32_t stack[kLbvhStack];
+    int top = 0;
+    stack[top++] = L.n_prims == 1 ? ~0 : 0;
+    while (top > 0) {
+        const int32_t node = stack[--top];
+        if (node < 0) {  // leaf: one region
+            const int reg = L.prims[~node];
+            const RegionRec rr = S.rec[reg];
+            double r_in, r_out;
+            slab_h(rr.lo, rr.hi, r, r_in, r_out);
+            const double ci = r_in > t_start ? r_in : t_start;
+            const double co = r_out < t_max ? r_out : t_max;
+            if (ci < co && (ci < best_in || (ci == best_in && reg < best_r))) {
+                best_r = reg;
+                best_in = ci;
+                best_out = co;
+            }
+            continue;
+        }
+        const LbvhNode nd = L.nodes[node];
+        double n_in, n_out;
+        slab_h(nd.lo, nd.hi, r, n_in, n_out);
+        const double lo_t = n_in > t_start ? n_in : t_start;
+        const double hi_t = n_out < t_max ? n_out : t_max;
+        if (lo_t >= hi_t || lo_t > best_in) continue;
+        // near child first (LIFO: push the far one first)
+        const int32_t *llo, *lhi, *rlo, *rhi;
+        lbvh_child_box(S, L, nd.left, llo, lhi);
+        lbvh_child_box(S, L, nd.right, rlo, rhi);
+        double l_in, l_out, q_in, q_out;
+        slab_h(llo, lhi, r, l_in, l_out);
+        slab_h(rlo, rhi, r, q_in, q_out);
+        if (top + 2 > kLbvhStack) __trap();  // depth checked at build time
+        if (l_in <= q_in) {
+            stack[top++] = nd.right;
+            stack[top++] = nd.left;
+        } else {
+            stack[top++] = nd.left;
+            stack[top++] = nd.right;
+        }
+    }
+    if (best_r < 0) return false;
+    rid = best_r;
+    c_in_o = best_in;
+    c_out_o = best_out;
+    return true;
+}
+
+// _bvh_point_query (R/accel.py:355-388): region whose half-open box holds p
+__device__ inline int lbvh_point(const SceneView& S, const LbvhView& L, double px, double py, double pz) {
+    if (L.n_prims == 0) return -1;
+    const double p[3] = {px, py, pz};
+    int32_t stack[kLbvhStack];
+    int top = 0;
+    stack[top++] = L.n_prims == 1 ? ~0 : 0;
+    while (top > 0) {
+        const int32_t node = stack[--top];
+        const int32_t *lo, *hi;
+        lbvh_child_box(S, L, node, lo, hi);
+        bool in = true;
+#pragma unroll
+        for (int a = 0; a < 3; a++) in = in && p[a] >= (double)lo[a] * 0.5 && p[a] < (double)hi[a] * 0.5;
+        if (!in) continue;
+        if (node < 0) return L.prims[~node];
+        if (top + 2 > kLbvhStack) __trap();
+        stack[top++] = L.nodes[node].right;
+        stack[top++] = L.nodes[node].left;
+    }
+    return -1;
+}
+
+
+// ---------------------------------------------------------------------------
 // reconstruction: _accumulate_bricks / _gradient_bricks fused in one gather
 // (R/sampling.py:57-103, 123-181).  GRAD=false: value only.
 
@@ -898,7 +1007,8 @@ __device__ __forceinline__ void count_eval(RayStats& st, int nids, const Accum& 
 // _iso_ray, R/render.py:456-518
 template <bool COUNT>
 __device__ bool iso_ray(const SceneView& S, const uint8_t* __restrict__ iflags, const MarchConst& M, const Ray& r,
-                        double tmin, double tmax, double rho, double& t_hit, double g[3], RayStats& st) {
+                        double tmin, double tmax, double rho, double& t_hit, double g[3], RayStats& st,
+                        const LbvhView* lb = nullptr) {
     KdWalk w;
     kd_begin(S, r, w);
     double t = tmin;
@@ -908,7 +1018,10 @@ __device__ bool iso_ray(const SceneView& S, const uint8_t* __restrict__ iflags, 
     for (;;) {
         int rid;
         double t_in, t_out;
-        if (!kd_next(S, iflags, r, w, t, tmax, rid, t_in, t_out)) return false;
+        // next region: ordered k-d walk, or a fresh LBVH closest-hit query (the reference's way)
+        if (!(lb ? lbvh_next_hit(S, *lb, r, t, tmax, rid, t_in, t_out)
+                 : kd_next(S, iflags, r, w, t, tmax, rid, t_in, t_out)))
+            return false;
         const RegionRec rr = S.rec[rid];
         const int nids = rr.meta & 0xffffff;
         const int32_t* ids = S.rids + rr.ids_begin;
@@ -964,7 +1077,7 @@ __device__ bool iso_ray(const SceneView& S, const uint8_t* __restrict__ iflags, 
 template <int GRAD, bool COUNT>
 __device__ void volume_ray(const SceneView& S, const uint8_t* __restrict__ vflags, const MarchConst& M,
                            const double* tf, const Ray& r, double tmin, double tmax, double rho, double acc[4],
-                           RayStats& st) {
+                           RayStats& st, const LbvhView* lb = nullptr) {
     double ar = 0.0, ag = 0.0, ab = 0.0, aa = 0.0;
     KdWalk w;
     kd_begin(S, r, w);
@@ -973,7 +1086,9 @@ __device__ void volume_ray(const SceneView& S, const uint8_t* __restrict__ vflag
     while (aa < M.early) {
         int rid;
         double t_in, t_out;
-        if (!kd_next(S, vflags, r, w, t, tmax, rid, t_in, t_out)) break;
+        if (!(lb ? lbvh_next_hit(S, *lb, r, t, tmax, rid, t_in, t_out)
+                 : kd_next(S, vflags, r, w, t, tmax, rid, t_in, t_out)))
+            break;
         st.regions++;
         const RegionRec rr = S.rec[rid];
         const int nids = rr.meta & 0xffffff;

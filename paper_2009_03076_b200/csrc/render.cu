@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(128) k_iso_pass(const __grid_constant__ Render
         t_end = tmax;
         if (tmin < tmax) {
             double g[3], th = 0.0;
-            if (iso_ray<COUNT>(A.S, A.iflags, A.M, r, tmin, tmax, rho, th, g, st)) {
+            if (iso_ray<COUNT>(A.S, A.iflags, A.M, r, tmin, tmax, rho, th, g, st, A.use_lbvh ? &A.ilb : nullptr)) {
                 t_end = th;
                 f = shade_factor(g, r);
             }
@@ -1175,7 +1175,8 @@ __global__ void __launch_bounds__(kTileW* kTileH) k_render(const __grid_constant
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         if (tmin < tmax) {
             double t_end = ISO ? A.iso_tend[slot] : tmax;
-            volume_ray<GRAD, COUNT>(A.S, A.vflags, A.M, s_tf, r, tmin, t_end, rho, acc, st);
+            volume_ray<GRAD, COUNT>(A.S, A.vflags, A.M, s_tf, r, tmin, t_end, rho, acc, st,
+                                    A.use_lbvh ? &A.vlb : nullptr);
             if (ISO && A.iso_shade[slot] >= 0.0) {
                 const double f = A.iso_shade[slot];
                 const double w = 1.0 - acc[3];
@@ -1232,6 +1233,8 @@ static FrameFn warp_fn(bool count) {
 
 // XB_KERNEL=frame | tile selects the per-lane kernels for A/B measurements
 static int kernel_choice() {
+    const char* tr = getenv("XB_TRAVERSAL");
+    if (tr && strcmp(tr, "lbvh") == 0) return 2;  // per-visit LBVH queries run in the one-thread-per-pixel kernel
     const char* e = getenv("XB_KERNEL");
     if (e && strcmp(e, "tile") == 0) return 2;
     if (e && strcmp(e, "frame") == 0) return 1;
@@ -1337,14 +1340,15 @@ __global__ void k_rays(const __grid_constant__ RayBatchArgs B) {
     double tmin = B.t0[q], tmax = B.t1[q];
     const double rho = B.rho[q];
     RayStats st = {0, 0, 0};
+    const LbvhView* vl = B.use_lbvh ? &B.vlb : nullptr;
     if (B.mode == 0) {  // volume integration
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         clip_ray(B.M, r, tmin, tmax);
         if (tmin < tmax) {
             switch (B.M.grad_mode) {
-                case 0: volume_ray<0, false>(B.S, B.vflags, B.M, s_tf, r, tmin, tmax, rho, acc, st); break;
-                case 1: volume_ray<1, false>(B.S, B.vflags, B.M, s_tf, r, tmin, tmax, rho, acc, st); break;
-                default: volume_ray<2, false>(B.S, B.vflags, B.M, s_tf, r, tmin, tmax, rho, acc, st); break;
+                case 0: volume_ray<0, false>(B.S, B.vflags, B.M, s_tf, r, tmin, tmax, rho, acc, st, vl); break;
+                case 1: volume_ray<1, false>(B.S, B.vflags, B.M, s_tf, r, tmin, tmax, rho, acc, st, vl); break;
+                default: volume_ray<2, false>(B.S, B.vflags, B.M, s_tf, r, tmin, tmax, rho, acc, st, vl); break;
             }
         }
         for (int c = 0; c < 4; c++) B.out[4 * q + c] = acc[c];
@@ -1352,7 +1356,7 @@ __global__ void k_rays(const __grid_constant__ RayBatchArgs B) {
         B.counts[2 * q + 1] = st.samples;
     } else {  // iso intersection
         double g[3], th = 0.0;
-        const bool hit = iso_ray<false>(B.S, B.iflags, B.M, r, tmin, tmax, rho, th, g, st);
+        const bool hit = iso_ray<false>(B.S, B.iflags, B.M, r, tmin, tmax, rho, th, g, st, B.use_lbvh ? &B.ilb : nullptr);
         B.out[4 * q] = th;
         for (int c = 0; c < 3; c++) B.out[4 * q + 1 + c] = g[c];
         B.counts[2 * q] = hit ? 1 : 0;

@@ -34,6 +34,8 @@ struct RenderArgs {
     unsigned long long* walk_counter;  // k_walk slot counter, then the hit-list length
     int32_t* hit_list;                 // slots k_walk found to meet an active region (k_warp's work)
     float walk_tau_stop;               // k_walk stops listing once the opacity minorant passes this depth
+    int use_lbvh;                      // XB_TRAVERSAL=lbvh: per-visit LBVH closest-hit queries (tile kernel)
+    LbvhView vlb, ilb;                 // LBVHs of the volume / iso active sets
     double* iso_tend;           // per slot: volume t_end (iso hit or clip end)
     double* iso_shade;          // per slot: headlight factor of the iso hit, < 0 when none
     double tf[1024];
@@ -45,6 +47,8 @@ struct RayBatchArgs {
     const uint8_t* iflags;
     MarchConst M;
     int mode;  // 0 volume (integrate_ray), 1 iso (iso_intersect)
+    int use_lbvh;
+    LbvhView vlb, ilb;
     int64_t n;
     const double *o, *d, *t0, *t1, *rho;
     double* out;       // (n,4): RGBA, or (t_hit, gx, gy, gz)

@@ -156,7 +156,10 @@ def test_oracle_scan_matches_golden_outside(xb, name):
 
 
 @pytest.mark.parametrize("name", ["smoke", "gauss_aniso", "c1"])
-def test_traversal_intervals_bit_exact(xb, name):
+@pytest.mark.parametrize("traversal", ["kd", "lbvh"])
+def test_traversal_intervals_bit_exact(xb, name, traversal):
+    """iterate_intervals (R/accel.py:414-424): the ordered k-d walk and the LBVH
+    per-visit closest-hit queries both reproduce the reference's intervals."""
     from paper_2009_03076_b200.accel import TransferFunction, build_all_regions_bvh, build_volume_bvh, trace_rays
 
     model, _, regions = _build(name)
@@ -166,13 +169,56 @@ def test_traversal_intervals_bit_exact(xb, name):
             bvh = build_all_regions_bvh(regions)
         else:
             bvh = build_volume_bvh(regions, TransferFunction(g["rays_pruned_domain"], g["rays_pruned_tf"]))
-        got = trace_rays(bvh, g[f"rays_{tag}_o"], g[f"rays_{tag}_d"], 0.0, 1e9)
+        got = trace_rays(bvh, g[f"rays_{tag}_o"], g[f"rays_{tag}_d"], 0.0, 1e9, traversal=traversal)
         off = g[f"rays_{tag}_off"]
         for q in range(len(off) - 1):
             s, e = off[q], off[q + 1]
             want = list(zip(g[f"rays_{tag}_tin"][s:e].tolist(), g[f"rays_{tag}_tout"][s:e].tolist(),
                             g[f"rays_{tag}_region"][s:e].tolist()))
             assert got[q] == want, f"{name}/{tag} ray {q}"
+
+
+@pytest.mark.parametrize("name", ["smoke", "gauss_aniso", "c1", "two_cell", "single", "hole_pair"])
+def test_lbvh_structure_and_point_queries(xb, name):
+    """LBVH (Morton + Karras + refit): a full binary tree over exactly the active
+    regions, every internal box the exact union of its children; point queries
+    equal the reference's region of each golden sample point (R/accel.py:355-388)."""
+    from paper_2009_03076_b200.accel import TransferFunction, build_all_regions_bvh, build_volume_bvh, point_query_batch
+
+    model, _, regions = _build(name)
+    vr = regions.value_range[:, 0] if len(regions) else np.zeros((0, 2))
+    sets = [build_all_regions_bvh(regions)]
+    if len(regions):
+        lo, hi = float(vr[:, 0].min()), float(vr[:, 1].max())
+        if hi > lo:  # a band TF leaves a strict subset active
+            rgba = np.zeros((256, 4))
+            rgba[100:160, 3] = 0.5
+            sets.append(build_volume_bvh(regions, TransferFunction((lo, hi), rgba)))
+    for bvh in sets:
+        lo_, hi_, left, right, start, count, prims = bvh._lbvh()
+        n = bvh.n_active
+        assert np.array_equal(np.sort(prims), bvh.prims)
+        if n == 0:
+            assert len(left) == 1 and count[0] == 0
+            continue
+        assert len(left) == 2 * n - 1
+        leaf = left < 0
+        assert leaf.sum() == n and np.all(count[leaf] == 1) and np.all(right[leaf] == -1)
+        assert np.array_equal(np.sort(start[leaf]), np.arange(n))
+        seen = np.zeros(2 * n - 1, int)
+        for i in np.nonzero(~leaf)[0]:
+            for c in (left[i], right[i]):
+                seen[c] += 1
+            assert np.array_equal(lo_[i], np.minimum(lo_[left[i]], lo_[right[i]]))
+            assert np.array_equal(hi_[i], np.maximum(hi_[left[i]], hi_[right[i]]))
+        assert seen[0] == 0 and np.all(seen[1:] == 1)  # a tree rooted at node 0
+        for k in np.nonzero(leaf)[0]:
+            r = prims[start[k]]
+            assert np.array_equal(lo_[k], regions.lo[r]) and np.array_equal(hi_[k], regions.hi[r])
+    g = golden_model(name)
+    if "pts" in g and len(regions):
+        got = point_query_batch(sets[0], g["pts"])
+        assert np.array_equal(got, g["pts_region"].astype(np.int32)), name
 
 
 # ---------------------------------------------------------------- frames
@@ -206,8 +252,9 @@ KERNEL_ENVS = {
     "warp_nowalk": {"XB_WALK": "0"},   # k_warp's frontier only
     "frame": {"XB_KERNEL": "frame"},   # per-lane persistent kernel
     "tile": {"XB_KERNEL": "tile"},     # one thread per pixel
+    "lbvh": {"XB_TRAVERSAL": "lbvh"},  # per-visit LBVH closest-hit queries (the reference's traversal)
 }
-_ENV_KEYS = ("XB_KERNEL", "XB_LEAF_CAP", "XB_WALK")
+_ENV_KEYS = ("XB_KERNEL", "XB_LEAF_CAP", "XB_WALK", "XB_TRAVERSAL")
 
 
 @pytest.fixture
@@ -384,7 +431,7 @@ def test_acceptance_million_cells_vs_oracle(xb):
     # repetition
     import os
 
-    for kern in ("tile", "frame", "warp_cap1", "warp_nowalk"):
+    for kern in ("tile", "frame", "warp_cap1", "warp_nowalk", "lbvh"):
         os.environ.update(KERNEL_ENVS[kern])
         try:
             u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)

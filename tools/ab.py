@@ -30,9 +30,12 @@ stream = torch.cuda.current_stream()
 
 def setv(v):
     """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N) | gD (guided grab divisor D)"""
-    for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU"):
+    for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU",
+              "XB_TRAVERSAL"):
         os.environ.pop(k, None)
-    if v == "notau":
+    if v == "lbvh":
+        os.environ["XB_TRAVERSAL"] = "lbvh"
+    elif v == "notau":
         os.environ["XB_WALK_NOTAU"] = "1"
     elif v == "nowalk":
         os.environ["XB_WALK"] = "0"
