@@ -496,10 +496,12 @@ def run_config(args, cfg, cfg_name, with_extras):
             "kernel_ms": ms_kernel, "wall_s_timed": wall,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_warp<1,false,false> (csrc/render.cu)",
+                         "kernel": "frame = k_classify + k_walk + k_warp<1,false,false> (csrc/render.cu); achieved over "
+                                   "the whole frame's event time",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6.65 TB/s"},
-            # our kernels per frame: k_warp (+ k_iso_pass) (+ k_unpack_tiles on rank 0 when tiled)
-            "gpu_launches": args.steps * (1 + (cfg.get("iso") is not None) + (world > 1)),
+            # our kernels per frame: k_classify, k_walk, k_warp (+ k_iso_pass) (+ k_unpack_tiles on rank 0
+            # when tiled); the CUB select between k_classify and k_walk is library code
+            "gpu_launches": args.steps * (3 + (cfg.get("iso") is not None) + (world > 1)),
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

@@ -538,13 +538,15 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             if (walk) {
                 keep_pool(m->m.device);
                 const char* ec = getenv("XB_LEAF_CAP");
-                const int cap = ec ? std::max(1, atoi(ec)) : 64;  // sweep: C2 64 ~ 128 ~ 384, C3 16 < 32 < 64 << 384
+                const int cap = ec ? std::max(1, atoi(ec)) : 48;  // sweep (with resume): C2 128 6.47, 64 6.62, 32 7.08 ms; C3 16 1.48, 32 1.52, 64 1.61, 128 1.98 ms
                 const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
                 const size_t ns1 = std::max<size_t>(n_slots, 1);
-                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 2) * sizeof(int32_t), s));
+                const size_t res_words = 1 + 3 * 48;  // render.cu kResume
+                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 2 + res_words) * sizeof(int32_t), s));
                 A->leaf_count = leaf_buf;
                 A->hit_list = leaf_buf + ns1;
-                A->leaves = leaf_buf + 2 * ns1;
+                A->resume = leaf_buf + 2 * ns1;
+                A->leaves = leaf_buf + (2 + res_words) * ns1;
                 A->leaf_cap = cap;
             }
         }

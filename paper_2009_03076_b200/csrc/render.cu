@@ -453,6 +453,7 @@ constexpr int kWalkThreads = 128;
 constexpr int kWalkStack = 100;  // >= 3 x (Kd4 depth <= kKdStack / 2 + 1)
 constexpr int kLeafCountMask = 0x3fffffff;
 constexpr int kLeafTruncated = 0x40000000;
+constexpr int kResume = 48;  // resume entries saved per truncated walk
 
 // pixel of a ray that meets no active region: transparent, or the iso colour
 __device__ __forceinline__ void write_empty_pixel(const RenderArgs& A, int64_t slot, int64_t out, bool clip_ok) {
@@ -467,6 +468,35 @@ __device__ __forceinline__ void write_empty_pixel(const RenderArgs& A, int64_t s
         }
     }
     write_pixel(A, out, acc, 0, 0);
+}
+
+// The ordered rest of a truncated walk — the pending entry (if any) followed by
+// the stack from top to bottom — is exactly a warp-frontier list (disjoint
+// subtrees in ray order, conservative float intervals): k_warp resumes from it
+// instead of re-descending from the root.  More than kResume entries: none
+// saved (k_warp restarts at the root, which is exact as well).
+constexpr int kNoEntry = 0x7fffffff;
+__device__ __forceinline__ void save_resume(const RenderArgs& A, int64_t slot, int code, double tn, double tf,
+                                            const int* st_code, const float* st_tn, const float* st_tf, int sp_n) {
+    int32_t* __restrict__ res = A.resume + slot * (int64_t)(1 + 3 * kResume);
+    const int m = (code != kNoEntry ? 1 : 0) + sp_n;
+    if (m > kResume) {
+        res[0] = -1;
+        return;
+    }
+    res[0] = m;
+    int k = 0;
+    if (code != kNoEntry) {
+        res[1 + 3 * k] = code;
+        res[2 + 3 * k] = __float_as_int(__double2float_rd(tn));
+        res[3 + 3 * k] = __float_as_int(__double2float_ru(tf));
+        k++;
+    }
+    for (int q = sp_n - 1; q >= 0; q--, k++) {
+        res[1 + 3 * k] = st_code[q];
+        res[2 + 3 * k] = __float_as_int(st_tn[q]);
+        res[3 + 3 * k] = __float_as_int(st_tf[q]);
+    }
 }
 
 // Rays that can meet an active region (root box hit after clipping) -> flag;
@@ -526,12 +556,20 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                 float tau = 0.f;
                 for (;;) {
                     if (code <= -2) {  // a leaf: list it
-                        if (count == A.leaf_cap) { flags = kLeafTruncated; break; }
+                        if (count == A.leaf_cap) {  // this leaf resumes the rest of the walk
+                            flags = kLeafTruncated;
+                            save_resume(A, slot, code, tn, tf, st_code, st_tn, st_tf, sp_n);
+                            break;
+                        }
                         const int rid = -2 - code;
                         out[count++] = rid;
                         if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
                             tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;
-                            if (tau > tau_stop) { flags = kLeafTruncated; break; }
+                            if (tau > tau_stop) {
+                                flags = kLeafTruncated;
+                                save_resume(A, slot, kNoEntry, 0.0, 0.0, st_code, st_tn, st_tf, sp_n);
+                                break;
+                            }
                         }
                     } else {
                         // expand the Kd4 node (same classification as kd_next / k_warp)
@@ -886,11 +924,31 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                                 walk = false;
                                 continue;
                             }
-                            n = 1;
-                            if (lane == 0) {
-                                e_code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
-                                e_tn = root_a;
-                                e_tf = root_b;
+                            const int32_t* res = A.resume + slot * (int64_t)(1 + 3 * kResume);
+                            const int m = res[0];
+                            if (m >= 0) {  // resume k_walk's ordered remainder: lanes take the first 32
+                                n = min(m, 32);
+                                if (lane < n) {
+                                    e_code = res[1 + 3 * lane];
+                                    e_tn = (double)__int_as_float(res[2 + 3 * lane]);
+                                    e_tf = (double)__int_as_float(res[3 + 3 * lane]);
+                                }
+                                if (m > 32) {  // the rest to the spill stack, earliest on top
+                                    spn = m - 32;
+                                    for (int q = lane; q < spn; q += 32) {
+                                        const int k = 32 + q;  // list entry k -> stack position spn-1-q
+                                        stk[spn - 1 - q] = SpillEnt{res[1 + 3 * k], __int_as_float(res[2 + 3 * k]),
+                                                                    __int_as_float(res[3 + 3 * k])};
+                                    }
+                                }
+                                __syncwarp();
+                            } else {
+                                n = 1;
+                                if (lane == 0) {
+                                    e_code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
+                                    e_tn = root_a;
+                                    e_tf = root_b;
+                                }
                             }
                             continue;
                         }

@@ -30,6 +30,7 @@ struct RenderArgs {
     int32_t* leaves;                   // k_walk -> k_warp: per slot leaf_cap region ids in ray order (or NULL)
     int32_t* leaf_count;               // per slot: count | 0x40000000 when truncated
     int leaf_cap;
+    int32_t* resume;                   // per slot: k_walk's ordered remainder when truncated (1 + 3 x kResume words)
     const float* vqmin;                // per region opacity minorant (k_walk early stop), may be NULL
     unsigned long long* walk_counter;  // k_walk slot counter, then the hit-list length
     int32_t* hit_list;                 // slots k_walk found to meet an active region (k_warp's work)

@@ -53,5 +53,5 @@ if __name__ == "__main__":
         for rh, rr in ((200, 412), (200, 420)):
             print("gear", rh, rr, run(gear(rh, rr), build), flush=True)
     else:
-        for thr, rh, rr in ((0.005, 80, 160), (0.003, 80, 240), (0.002, 80, 280), (0.002, 80, 300), (0.0015, 80, 300)):
-            print("jet", thr, rh, rr, run(jet(thr, rh, rr), build), flush=True)
+        for thr, rh, rr in ((0.0027, 80, 240), (0.0026, 80, 240), (0.0025, 80, 240), (0.003, 80, 260)):
+            print("jet", thr, rh, rr, run(jet(thr, rh, rr), False), flush=True)

@@ -15,37 +15,47 @@ def main():
     rep = sys.argv[1]
     rows = ncu_csv(rep, "details")
     h = rows[0]
-    k_i, s_i, m_i, u_i, v_i = (h.index(x) for x in ("Kernel Name", "Section Name", "Metric Name", "Metric Unit",
-                                                    "Metric Value"))
+    k_i, m_i, u_i, v_i = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Unit", "Metric Value"))
+    id_i = h.index("ID")
     keep = ("Duration", "SM Frequency", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate", "L2 Hit Rate",
             "Compute (SM) Throughput", "Executed Ipc Active", "Issue Slots Busy", "Registers Per Thread",
             "Achieved Occupancy", "Theoretical Occupancy", "Avg. Active Threads Per Warp",
             "Warp Cycles Per Issued Instruction", "Eligible Warps Per Scheduler", "Executed Instructions",
             "Branch Efficiency", "Grid Size", "Block Size", "Stack Size")
     print(f"# ncu --set full summary: {rep}")
-    print(f"kernel: {rows[1][k_i]}")
-    for r in rows[1:]:
-        if r[m_i] in keep:
-            print(f"  {r[m_i]:40s} {r[v_i]:>16s} {r[u_i]}")
     raw = ncu_csv(rep, "raw")
-    d = dict(zip(raw[0], raw[2]))
-    u = dict(zip(raw[0], raw[1]))
-    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "l1tex__t_bytes.sum",
-              "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
-              "smsp__thread_inst_executed.sum"):
-        if k in d:
-            print(f"  {k:60s} {d[k]:>16s} {u.get(k, '')}")
-    st = []
-    for k, v in d.items():
-        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
-            try:
-                st.append((float(v.replace(",", "")), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
-            except ValueError:
-                pass
-    tot = sum(v for v, _ in st) or 1
-    print("  warp stall samples (share):")
-    for v, k in sorted(st, reverse=True)[:10]:
-        print(f"    {k:28s} {100 * v / tot:5.1f} %")
+    rh = raw[0]
+    ids = []
+    for r in rows[1:]:
+        if r[id_i] not in ids:
+            ids.append(r[id_i])
+    for kid in ids:
+        kr = [r for r in rows[1:] if r[id_i] == kid]
+        print(f"kernel: {kr[0][k_i]}")
+        for r in kr:
+            if r[m_i] in keep:
+                print(f"  {r[m_i]:40s} {r[v_i]:>16s} {r[u_i]}")
+        rr = [x for x in raw[2:] if x[rh.index("ID")] == kid]
+        if not rr:
+            continue
+        d = dict(zip(rh, rr[0]))
+        u = dict(zip(rh, raw[1]))
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum", "l1tex__t_bytes.sum",
+                  "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+                  "smsp__thread_inst_executed.sum"):
+            if k in d:
+                print(f"  {k:60s} {d[k]:>16s} {u.get(k, '')}")
+        st = []
+        for k, v in d.items():
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+                try:
+                    st.append((float(v.replace(",", "")), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
+                except ValueError:
+                    pass
+        tot = sum(v for v, _ in st) or 1
+        print("  warp stall samples (share):")
+        for v, k in sorted(st, reverse=True)[:8]:
+            print(f"    {k:28s} {100 * v / tot:5.1f} %")
     if len(sys.argv) > 2:
         rows = list(csv.reader(open(sys.argv[2])))
         hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)

@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep = sys.argv[1]
 pref = sys.argv[2] if len(sys.argv) > 2 else "_ZN2xb6k_warpILi1ELb0ELb0ELi4E"
 out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "sass_lines.py"), rep, pref, "-", "100000"],
-                     capture_output=True, text=True).stdout
+                     capture_output=True, text=True, env=dict(os.environ, XB_NCU_KERNEL="k_warp")).stdout
 rows = []
 for ln in out.splitlines()[1:]:
     p = ln.split()

@@ -18,9 +18,11 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def sass_csv(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+def sass_csv(rep, kfilter=None):
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+    if kfilter:
+        cmd += ["-k", "regex:" + kfilter]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
     return hdr, rows[2:]
@@ -55,7 +57,8 @@ def main():
                        cwd=d, capture_output=True)
         cubin = os.path.join(d, "render.sm_100a.cubin")
     lm = line_map(cubin, prefix)
-    hdr, rows = sass_csv(rep)
+    kf = os.environ.get("XB_NCU_KERNEL")  # e.g. k_warp when the report holds several kernels
+    hdr, rows = sass_csv(rep, kf)
     ia, ist, iex = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index(
         "Instructions Executed")
     ith = hdr.index("Thread Instructions Executed")
