@@ -62,9 +62,9 @@ CONFIGS = {
                         "1920x1080, with a TF-edit active-set/majorant refresh"),
     # C5: Exajet-shaped, 4 levels, hole/refine chain along x (SURVEY.md §8(d) template)
     "c5": dict(spec="jet", gpu_gen=True, res=(1920, 1080), max_alpha=0.5, gradient="analytic",
-               workload="configs[4]: synthetic Exajet-shaped AMR (4 levels), 1920x1080 DVR + analytic shading"),
+               workload="configs[4]: synthetic Exajet-shaped AMR (4 levels, 647M cells), 1920x1080 DVR + analytic shading"),
 }
-JET = dict(thr=0.0027, rh=80.0, rr=240.0, step=80.0, sigma=400.0)
+JET = dict(thr=0.003, rh=80.0, rr=300.0, step=80.0, sigma=400.0)  # 647,115,612 cells (tools/calib.py)
 
 
 def spec_for(cfg):

@@ -53,5 +53,5 @@ if __name__ == "__main__":
         for rh, rr in ((200, 412), (200, 420)):
             print("gear", rh, rr, run(gear(rh, rr), build), flush=True)
     else:
-        for thr, rh, rr in ((0.0027, 80, 240), (0.0026, 80, 240), (0.0025, 80, 240), (0.003, 80, 260)):
+        for thr, rh, rr in ((0.0029, 80, 240), (0.0028, 80, 240), (0.003, 80, 290), (0.003, 80, 300)):
             print("jet", thr, rh, rr, run(jet(thr, rh, rr), False), flush=True)

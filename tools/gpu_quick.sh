@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_parity.py -q -m gpu -x --timeout 900 -k "acceptance or frames_match" > gpurun_out/pt_res1.log 2>&1; tail -1 gpurun_out/pt_res1.log
-timeout 300 python tools/ab.py c2 warp,cap16,cap32,cap128,nowalk 6 > gpurun_out/ab_res1.log 2>&1; grep median gpurun_out/ab_res1.log
-timeout 300 python tools/ab.py c3 warp,cap16,cap32,cap128,nowalk 6 > gpurun_out/ab_res1c3.log 2>&1; grep median gpurun_out/ab_res1c3.log
+for c in c5 c4; do timeout 1200 python bench.py --config $c --secondary '' --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; python -c "
+import json; d=json.loads(open('gpurun_out/bench_$c.json').read().strip().splitlines()[-1]); c=d['config']
+print('$c', d['value'], d['ms_per_step'], d['msamples_per_s'], c['cells'], c['bricks'], c['regions'], c['build_ms'], c.get('tf_refresh_ms'), d['frame']['samples'], d['e2e']['value'], (d['cpu_baseline'] or {}).get('value'))"; tail -2 gpurun_out/bench_$c.err; done
+nvidia-smi --query-gpu=memory.used,memory.total --format=csv
