@@ -88,6 +88,10 @@ int xb_model_download(const xb_model* m, int32_t* lower, int32_t* level, int32_t
 int xb_model_download_tree(const xb_model* m, int32_t* axis, double* pos, int32_t* left, int32_t* right,
                            int32_t* brick_start, int32_t* brick_count, double* box_lo, double* box_hi,
                            double* max_half);
+/* attach SplitTree arrays (R/bricks.py:45-68) to a model, e.g. one created with xb_model_upload */
+int xb_model_upload_tree(xb_model* m, int64_t n, const int32_t* axis, const double* pos, const int32_t* left,
+                         const int32_t* right, const int32_t* brick_start, const int32_t* brick_count,
+                         const double* box_lo, const double* box_hi, const double* max_half);
 void xb_model_free(xb_model* m);
 
 /* ---- regions: build_regions(model) R/regions.py:90-213 ---- */
@@ -128,6 +132,7 @@ typedef struct {
     double iso_rgb[3]; /* ISO_COLOR, R/render.py:47 */
     double tf_lo, tf_hi;
     double tf_rgba[1024];
+    int32_t use_tree; /* render_frame(use_celllocation=True): per-sample split-tree brick collection */
 } xb_march;
 
 /* Render the tiles of `tile_rank` out of `tile_world` (16x8-pixel tiles dealt

@@ -42,7 +42,8 @@ class XbCamera(C.Structure):
 class XbMarch(C.Structure):
     _fields_ = [("samples_per_cell", f64), ("rate_scale", f64), ("early_term_threshold", f64), ("seed", u64),
                 ("gradient_mode", i32), ("n_planes", i32), ("planes", (f64 * 4) * 6), ("iso_on", i32),
-                ("iso_value", f64), ("iso_rgb", f64 * 3), ("tf_lo", f64), ("tf_hi", f64), ("tf_rgba", f64 * 1024)]
+                ("iso_value", f64), ("iso_rgb", f64 * 3), ("tf_lo", f64), ("tf_hi", f64), ("tf_rgba", f64 * 1024),
+                ("use_tree", i32)]
 
 
 class XbSynthSpec(C.Structure):
@@ -67,6 +68,7 @@ SIGNATURES = {
     "xb_model_info": (C.c_int, [P, P, P, P, P]),
     "xb_model_download": (C.c_int, [P, P, P, P, P, P]),
     "xb_model_download_tree": (C.c_int, [P, P, P, P, P, P, P, P, P, P]),
+    "xb_model_upload_tree": (C.c_int, [P, i64, P, P, P, P, P, P, P, P, P]),
     "xb_model_free": (None, [P]),
     "xb_build_regions": (C.c_int, [P, P]),
     "xb_regions_info": (C.c_int, [P, P, P, P, P]),

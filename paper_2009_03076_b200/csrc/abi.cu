@@ -104,6 +104,9 @@ xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
         S.root_hi[a] = r->r.root_hi[a];
     }
     S.n_kd = r->r.n_regions > 0 ? r->r.n_kd : 0;
+    const xb::DevModel& d = m->m;
+    S.tree = xb::TreeView{d.t_axis.p, d.t_left.p, d.t_right.p, d.t_bstart.p, d.t_bcount.p, d.t_lo.p, d.t_hi.p,
+                          d.t_mh.p, d.n_tree};
     S.n_kd4 = r->r.n_regions > 0 ? r->r.n_kd4 : 0;
     return S;
 }
@@ -125,6 +128,7 @@ void fill_march(xb::MarchConst& M, const xb_march* mp) {
     M.tf_lo = mp->tf_lo;
     M.tf_hi = mp->tf_hi;
     M.tf_inv = 1.0 / (mp->tf_hi - mp->tf_lo);
+    M.use_tree = mp->use_tree;
     for (int l = 0; l < 32; l++) {
         const double fw = std::ldexp(1.0, l);
         M.lv_dt[l] = fw / (M.spc * M.rate);
@@ -283,6 +287,28 @@ int xb_model_upload(const int32_t* lower, const int32_t* level, const int32_t* d
         xb::finish_model(m, st.s);
         XB_CUDA(cudaStreamSynchronize(st.s));
         *out = h.release();
+    });
+}
+
+int xb_model_upload_tree(xb_model* m, int64_t n, const int32_t* axis, const double* pos, const int32_t* left,
+                         const int32_t* right, const int32_t* brick_start, const int32_t* brick_count,
+                         const double* box_lo, const double* box_hi, const double* max_half) {
+    return guarded([&] {
+        XB_CHECK(m && n >= 0, XB_ERR_ARG, "bad tree upload");
+        xb::DeviceGuard g(m->m.device);
+        OwnedStream st;
+        xb::DevModel& d = m->m;
+        d.n_tree = n;
+        d.t_axis.upload(axis, n, st.s);
+        d.t_pos.upload(pos, n, st.s);
+        d.t_left.upload(left, n, st.s);
+        d.t_right.upload(right, n, st.s);
+        d.t_bstart.upload(brick_start, n, st.s);
+        d.t_bcount.upload(brick_count, n, st.s);
+        d.t_lo.upload(box_lo, 3 * n, st.s);
+        d.t_hi.upload(box_hi, 3 * n, st.s);
+        d.t_mh.upload(max_half, n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
     });
 }
 
@@ -468,6 +494,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         check_active(vol, r, "volume");
         A->vflags = vol->a.flags.p;
         A->vmask4 = vol->a.mask4.p;
+        XB_CHECK(!mp->use_tree || m->m.n_tree > 0, XB_ERR_NO_TREE,
+                 "cell-location sampling requires a model with the split tree");
         A->use_lbvh = 0;
         {
             const char* tr = getenv("XB_TRAVERSAL");

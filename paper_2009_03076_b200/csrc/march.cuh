@@ -70,7 +70,16 @@ __device__ __forceinline__ void slab_h(const int32_t* lo_h, const int32_t* hi_h,
     tmax_o = tmax;
 }
 
+// the brick build's split tree (SplitTree, R/bricks.py:45-68), preorder, for
+// the cell-location gather (use_celllocation); null when absent
+struct TreeView {
+    const int32_t *axis, *left, *right, *bstart, *bcount;
+    const double *lo, *hi, *mh;  // (n,3) boxes, max half cell width
+    int64_t n;
+};
+
 struct SceneView {
+    TreeView tree;
     const int4* __restrict__ brick_a;
     const uint32_t* __restrict__ brick_m;
     const float* __restrict__ vals;
@@ -902,6 +911,46 @@ __device__ __forceinline__ void tf_eval_fast(const double* tf, double tf_lo, dou
 // few ulp of pow, and a fraction of pow's code size
 __device__ __forceinline__ double opacity_correct(double a, double y) { return -expm1(y * log(1.0 - a)); }
 
+// _collect_bricks (R/sampling.py:184-224): ids of the bricks in every split-tree
+// leaf whose subtree box, dilated by its largest half cell width, holds p —
+// a superset of the bricks whose supports contain p — sorted ascending.  The
+// gather over them skips zero-weight cells exactly as over a region's list,
+// so both give the same floats.  Returns -1 if more than `cap` ids.
+constexpr int kTreeIds = 128;
+__device__ inline int collect_bricks(const TreeView& T, double px, double py, double pz, int32_t* out, int cap) {
+    int n = 0;
+    int32_t stack[128];
+    int top = 0;
+    stack[top++] = 0;
+    while (top > 0) {
+        const int nd = stack[--top];
+        const double e = T.mh[nd];
+        if (px <= T.lo[3 * nd] - e || px >= T.hi[3 * nd] + e || py <= T.lo[3 * nd + 1] - e ||
+            py >= T.hi[3 * nd + 1] + e || pz <= T.lo[3 * nd + 2] - e || pz >= T.hi[3 * nd + 2] + e)
+            continue;
+        if (T.axis[nd] < 0) {
+            for (int b = T.bstart[nd]; b < T.bstart[nd] + T.bcount[nd]; b++) {
+                if (n == cap) return -1;
+                out[n++] = b;
+            }
+        } else {
+            if (top + 2 > 128) return -1;
+            stack[top++] = T.right[nd];
+            stack[top++] = T.left[nd];
+        }
+    }
+    for (int a = 1; a < n; a++) {  // insertion sort (small sets)
+        const int32_t key = out[a];
+        int c = a - 1;
+        while (c >= 0 && out[c] > key) {
+            out[c + 1] = out[c];
+            c--;
+        }
+        out[c + 1] = key;
+    }
+    return n;
+}
+
 // central / clamped-central gradient (R/render.py:307-376)
 __device__ inline void central_gradient(const SceneView& S, int mode, double px, double py, double pz, int rid,
                                         const int32_t* ids, int nids, double val, double g[3], int64_t* n_evals) {
@@ -973,6 +1022,7 @@ struct MarchConst {
     // as the kernel would compute): dt = fw/(spc*rate), s1 = fw/spc (R/render.py:402-403)
     double lv_dt[32], lv_s1[32], lv_is1[32];
     double tf_inv;  // 1/(tf_hi - tf_lo)
+    int use_tree;   // cell-location gather through the split tree (render_frame(use_celllocation=True))
 };
 
 struct RayStats {
@@ -1110,7 +1160,14 @@ __device__ void volume_ray(const SceneView& S, const uint8_t* __restrict__ vflag
             prev = tk;
             st.samples++;
             const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1], pz = r.o[2] + mid * r.d[2];
-            gather<GRAD == 1>(S, ids, nids, px, py, pz, A);
+            if (M.use_tree && S.tree.n > 0) {  // cell location (R/render.py:423-425)
+                int32_t tids[kTreeIds];
+                const int tn = collect_bricks(S.tree, px, py, pz, tids, kTreeIds);
+                if (tn >= 0) gather<GRAD == 1>(S, tids, tn, px, py, pz, A);
+                else gather<GRAD == 1>(S, ids, nids, px, py, pz, A);  // same floats, see collect_bricks
+            } else {
+                gather<GRAD == 1>(S, ids, nids, px, py, pz, A);
+            }
             count_eval<COUNT>(st, nids, A);
             if (A.den > kEpsWeight) {
                 const double v = A.num / A.den;

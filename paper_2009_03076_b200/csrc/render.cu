@@ -1309,7 +1309,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         const void* fn = count ? (const void*)k_iso_pass<true> : (const void*)k_iso_pass<false>;
         XB_CUDA(cudaLaunchKernel(fn, dim3(grid_for(n_slots, 128)), dim3(128), args, 0, s));
     }
-    const int kc = kernel_choice();
+    const int kc = A.M.use_tree ? 2 : kernel_choice();  // cell location: the one-thread-per-pixel kernel
     {  // k_warp guided ray-grab schedule (tuning knob XB_GRAB_DIV)
         RenderArgs& W = const_cast<RenderArgs&>(A);
         W.grab_div = getenv("XB_GRAB_DIV") ? std::max(1, atoi(getenv("XB_GRAB_DIV"))) : 4;

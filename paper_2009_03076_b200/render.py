@@ -212,8 +212,9 @@ def camera_struct(camera: Camera) -> N.XbCamera:
     return c
 
 
-def march_struct(tf: TransferFunction, params: MarchParams, iso_value=None) -> N.XbMarch:
+def march_struct(tf: TransferFunction, params: MarchParams, iso_value=None, use_tree=False) -> N.XbMarch:
     m = N.XbMarch()
+    m.use_tree = int(bool(use_tree))
     m.samples_per_cell = float(params.samples_per_cell)
     m.rate_scale = float(params.rate_scale)
     m.early_term_threshold = float(params.early_term_threshold)
@@ -245,8 +246,24 @@ def _scene_handles(scene: Scene):
     return rh.model_handle, rh, vb.handle, ib, iso_on
 
 
+def _ensure_device_tree(scene: Scene, mh) -> None:
+    """The model handle carries the split tree for the cell-location gather;
+    attach the scene's SplitTree when the handle was built without one."""
+    nb, nc, nf, nt = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int64()
+    N.check(N.lib().xb_model_info(mh.h, C.byref(nb), C.byref(nc), C.byref(nf), C.byref(nt)))
+    if nt.value > 0:
+        return
+    t = scene.tree
+    arr = lambda a, dt: np.ascontiguousarray(a, dt)  # noqa: E731
+    keep = [arr(t.axis, np.int32), arr(t.pos, np.float64), arr(t.left, np.int32), arr(t.right, np.int32),
+            arr(t.brick_start, np.int32), arr(t.brick_count, np.int32), arr(t.box_lo, np.float64),
+            arr(t.box_hi, np.float64), arr(t.max_half, np.float64)]
+    N.check(N.lib().xb_model_upload_tree(mh.h, len(keep[0]), *(N.ptr(a) for a in keep)))
+
+
 def render_native(scene: Scene, camera: Camera, tf: TransferFunction, params: MarchParams, out8, outf=None,
-                  counts=None, tile_rank=0, tile_world=1, count_bytes=False, stream=None, sync=True):
+                  counts=None, tile_rank=0, tile_world=1, count_bytes=False, stream=None, sync=True,
+                  use_celllocation=False):
     """One `xb_render` call; outputs may be numpy arrays or device pointers (ints).
 
     Returns [regions, samples, algorithmic bytes].  With sync=False and device
@@ -255,8 +272,12 @@ def render_native(scene: Scene, camera: Camera, tf: TransferFunction, params: Ma
     if camera.width < 1 or camera.height < 1:
         raise ValueError("image must be at least 1x1 pixel")
     mh, rh, vh, ih, iso_on = _scene_handles(scene)
+    if use_celllocation:
+        if scene.tree is None:
+            raise ValueError("cell-location sampling requires a scene built with the split tree")
+        _ensure_device_tree(scene, mh)
     cam = camera_struct(camera)
-    m = march_struct(tf, params, scene.iso_value if iso_on else None)
+    m = march_struct(tf, params, scene.iso_value if iso_on else None, use_tree=use_celllocation)
     stats = np.zeros(3, np.int64) if (sync or count_bytes) else None
     N.check(N.lib().xb_render(mh.h, rh.h, int(scene.field), vh.h, ih.h if ih else None, C.byref(cam), C.byref(m),
                               int(tile_rank), int(tile_world), N.ptr(out8), N.ptr(outf), N.ptr(counts), N.ptr(stats),
@@ -268,9 +289,10 @@ def render_frame(scene: Scene, camera: Camera, tf: TransferFunction, params: Mar
                  use_celllocation: bool = False) -> Frame:
     """Render a full frame on the GPU (R/render.py:654-691).
 
-    `use_celllocation` selects the reference's per-sample split-tree lookup,
-    whose frames are pixel-identical to the region path by construction
-    (R/render.py:657-659); on the GPU both requests run the region path.
+    `use_celllocation` selects the reference's per-sample split-tree lookup
+    (R/render.py:423-425, `_collect_bricks` R/sampling.py:184-224) — the paper's
+    cell-location baseline, run by the one-thread-per-pixel kernel; its frames
+    are pixel-identical to the region path by construction (R/render.py:657-659).
     """
     if camera.width < 1 or camera.height < 1:
         raise ValueError("image must be at least 1x1 pixel")
@@ -278,18 +300,20 @@ def render_frame(scene: Scene, camera: Camera, tf: TransferFunction, params: Mar
         raise ValueError("cell-location sampling requires a scene built with the split tree")
     t0 = time.perf_counter()
     out = np.empty((camera.height, camera.width, 4), np.uint8)
-    stats = render_native(scene, camera, tf, params, out)
+    stats = render_native(scene, camera, tf, params, out, use_celllocation=use_celllocation)
     ms = (time.perf_counter() - t0) * 1000.0
     return Frame(camera.width, camera.height, out, FrameStats(ms, int(stats[0]), int(stats[1])))
 
 
-def render_frame_float(scene: Scene, camera: Camera, tf: TransferFunction, params: MarchParams, count_bytes=False):
+def render_frame_float(scene: Scene, camera: Camera, tf: TransferFunction, params: MarchParams, count_bytes=False,
+                       use_celllocation=False):
     """Parity variant: (RGBA8, float64 RGBA before quantisation, per-pixel (regions, samples), stats)."""
     H, W = camera.height, camera.width
     out = np.empty((H, W, 4), np.uint8)
     outf = np.empty((H, W, 4), np.float64)
     cnt = np.empty((H, W, 2), np.int32)
-    stats = render_native(scene, camera, tf, params, out, outf, cnt, count_bytes=count_bytes)
+    stats = render_native(scene, camera, tf, params, out, outf, cnt, count_bytes=count_bytes,
+                          use_celllocation=use_celllocation)
     return out, outf, cnt, stats
 
 

@@ -296,6 +296,45 @@ def test_frames_match_reference(xb, key, frames, kernel_env):
     assert fr.stats.regions == int(frames[f"{key}_px_regions"].sum())
 
 
+@pytest.mark.parametrize("key", _frame_keys())
+def test_cell_location_frames_match_reference(xb, key, frames):
+    """use_celllocation=True: per-sample split-tree brick collection (the paper's
+    cell-location baseline, R/render.py:423-425) gives the reference's frames."""
+    from paper_2009_03076_b200.accel import TransferFunction
+    from paper_2009_03076_b200.render import build_scene, render_frame_float
+
+    meta = frame_meta(frames, key)
+    model, tree, regions = _build(FRAME_MODEL[key.split("_")[0]], keep_tree=True)
+    tf = TransferFunction(meta["tf_domain"], frames[f"{key}_tf_rgba"])
+    scene = build_scene(model, regions, tf, iso_value=meta["iso"], tree=tree)
+    u8, f64, cnt, stats = render_frame_float(scene, _camera(meta), tf, _params(meta), use_celllocation=True)
+    assert np.abs(f64 - frames[f"{key}_rgba_f64"]).max() <= RGBA_TOL
+    assert np.array_equal(cnt[..., 0].ravel(), frames[f"{key}_px_regions"])
+    assert np.array_equal(cnt[..., 1].ravel(), frames[f"{key}_px_samples"])
+
+
+def test_cell_location_uploaded_tree(xb):
+    """A model uploaded from arrays gets the scene's SplitTree attached on demand."""
+    from paper_2009_03076_b200.accel import TransferFunction
+    from paper_2009_03076_b200.model import AmrModel
+    from paper_2009_03076_b200.orbit import orbit_cameras
+    from paper_2009_03076_b200.regions import build_regions
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame, render_frame_float
+
+    model, tree, _ = _build("smoke", keep_tree=True)
+    m2 = AmrModel(model.field_names, model.brick_lower, model.brick_level, model.brick_dims, model.scalars)
+    regions = build_regions(m2)
+    lo, hi = m2.value_range(0)
+    tf = TransferFunction.grayscale((lo, hi), max_alpha=0.5)
+    scene = build_scene(m2, regions, tf, tree=tree)
+    cam = orbit_cameras(regions.bounds, 1, 64, 48)[0]
+    p = MarchParams(seed=3, gradient_mode="analytic")
+    a = render_frame_float(scene, cam, tf, p)
+    b = render_frame_float(scene, cam, tf, p, use_celllocation=True)
+    assert np.array_equal(a[2], b[2]) and np.abs(a[1] - b[1]).max() <= RGBA_TOL
+    assert np.array_equal(render_frame(scene, cam, tf, p).rgba, render_frame(scene, cam, tf, p, True).rgba)
+
+
 # ---------------------------------------------------------------- acceptance properties (T/test_acceptance.py)
 
 

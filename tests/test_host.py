@@ -40,7 +40,22 @@ def test_struct_layouts_match_header():
 
     # xb_camera: 2 ints + 12 doubles + 2 doubles; xb_march per the header
     assert ctypes.sizeof(N.XbCamera) == 8 + 14 * 8
-    assert ctypes.sizeof(N.XbMarch) == 3 * 8 + 8 + 8 + 24 * 8 + 8 + 8 + 3 * 8 + 16 + 1024 * 8
+    assert ctypes.sizeof(N.XbMarch) == 3 * 8 + 8 + 8 + 24 * 8 + 8 + 8 + 3 * 8 + 16 + 1024 * 8 + 8  # + use_tree (padded)
+
+
+def test_struct_sizes_match_c_compiler(tmp_path):
+    """ctypes mirrors of xb_camera / xb_march / xb_synth_spec match gcc's layout of include/exabricks.h."""
+    import subprocess
+
+    from paper_2009_03076_b200 import _native as N
+
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "exabricks.h"\nint main(void){printf("%zu %zu %zu\\n",'
+                   'sizeof(xb_camera), sizeof(xb_march), sizeof(xb_synth_spec));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got == [ctypes.sizeof(N.XbCamera), ctypes.sizeof(N.XbMarch), ctypes.sizeof(N.XbSynthSpec)]
 
 
 def test_compute_fails_loudly_without_device():
