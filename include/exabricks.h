@@ -69,6 +69,11 @@ int xb_cells_info(const xb_cells* c, int64_t* n);
 /* host arrays of length n: CellList.i/j/k/level (int32) and values (float32, one field) */
 int xb_cells_download(const xb_cells* c, int32_t* i, int32_t* j, int32_t* k, int32_t* level, float* values);
 void xb_cells_free(xb_cells* c);
+/* streamed input (io.load_cells_device: .exacells read in chunks, R/io.py:88-113): allocate n cells on
+ * `device`, then fill [offset, offset + count) from host or device arrays */
+int xb_cells_create(int64_t n, int32_t device, xb_cells** out);
+int xb_cells_upload(xb_cells* c, int64_t offset, int64_t count, const int32_t* i, const int32_t* j, const int32_t* k,
+                    const int32_t* level, const float* values);
 /* build_bricks on device-resident cells (same result as xb_build_bricks on the downloaded arrays) */
 int xb_build_bricks_cells(const xb_cells* c, int32_t max_brick_width, int32_t keep_split_tree, xb_model** out);
 

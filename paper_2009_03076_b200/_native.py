@@ -62,6 +62,8 @@ SIGNATURES = {
     "xb_cells_info": (C.c_int, [P, P]),
     "xb_cells_download": (C.c_int, [P, P, P, P, P, P]),
     "xb_cells_free": (None, [P]),
+    "xb_cells_create": (C.c_int, [i64, i32, P]),
+    "xb_cells_upload": (C.c_int, [P, i64, i64, P, P, P, P, P]),
     "xb_build_bricks_cells": (C.c_int, [P, i32, i32, P]),
     "xb_build_bricks": (C.c_int, [P, P, P, P, P, i64, i32, i32, i32, i32, P]),
     "xb_model_upload": (C.c_int, [P, P, P, P, i64, i64, i32, i32, P]),

@@ -247,6 +247,38 @@ int xb_cells_download(const xb_cells* c, int32_t* i, int32_t* j, int32_t* k, int
 
 void xb_cells_free(xb_cells* c) { delete c; }
 
+int xb_cells_create(int64_t n, int32_t device, xb_cells** out) {
+    *out = nullptr;
+    return guarded([&] {
+        XB_CHECK(n >= 0 && n < (1ll << 31) - 2, XB_ERR_RANGE, "cell count out of range");
+        xb::DeviceGuard g(device);
+        auto h = std::make_unique<xb_cells>();
+        h->c.device = device;
+        h->c.n = n;
+        h->c.i.alloc(n + 1); h->c.j.alloc(n + 1); h->c.k.alloc(n + 1); h->c.level.alloc(n + 1);
+        h->c.vals.alloc(n + 1);
+        *out = h.release();
+    });
+}
+
+int xb_cells_upload(xb_cells* c, int64_t offset, int64_t count, const int32_t* i, const int32_t* j, const int32_t* k,
+                    const int32_t* level, const float* values) {
+    return guarded([&] {
+        XB_CHECK(c && offset >= 0 && count >= 0 && offset + count <= c->c.n, XB_ERR_ARG, "upload range out of bounds");
+        xb::DeviceGuard g(c->c.device);
+        OwnedStream st;
+        const size_t b4 = (size_t)count * 4;
+        if (count) {
+            XB_CUDA(cudaMemcpyAsync(c->c.i.p + offset, i, b4, cudaMemcpyDefault, st.s));
+            XB_CUDA(cudaMemcpyAsync(c->c.j.p + offset, j, b4, cudaMemcpyDefault, st.s));
+            XB_CUDA(cudaMemcpyAsync(c->c.k.p + offset, k, b4, cudaMemcpyDefault, st.s));
+            XB_CUDA(cudaMemcpyAsync(c->c.level.p + offset, level, b4, cudaMemcpyDefault, st.s));
+            XB_CUDA(cudaMemcpyAsync(c->c.vals.p + offset, values, b4, cudaMemcpyDefault, st.s));
+        }
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
 int xb_build_bricks_cells(const xb_cells* c, int32_t max_brick_width, int32_t keep_split_tree, xb_model** out) {
     *out = nullptr;
     return guarded([&] {

@@ -83,3 +83,27 @@ def test_landing_gear_shape_generates_all_levels():
     assert lv[0] > 4_000_000 and lv[12] > 0 and lv.sum() == len(a), lv
     c = np.stack([a.i, a.j, a.k], 1).astype(np.float64) + (2.0 ** a.level)[:, None] / 2
     assert not np.any(np.sum((c - 6144.0) ** 2, axis=1) < 60.0 ** 2)  # the hole is empty
+
+
+def test_streamed_exacells_loader(tmp_path):
+    """io.load_cells_device streams a .exacells file to the GPU in chunks
+    (R/io.py:88-113 format): same cells as load_cells, same bricks."""
+    from paper_2009_03076_b200 import io as xio
+    from paper_2009_03076_b200.bricks import build_bricks
+
+    cl = xio.generate_synthetic(spec_from_digest(DIG["gauss_aniso"]))
+    path = tmp_path / "m.exacells"
+    xio.save_cells(path, cl)
+    for chunk in (1000, 1 << 24):  # many chunks / one chunk
+        dc = xio.load_cells_device(path, chunk=chunk)
+        back = dc.to_host()
+        for a in ("i", "j", "k", "level", "values"):
+            assert np.array_equal(getattr(back, a), getattr(cl, a)), (chunk, a)
+    m_dev, _ = build_bricks(dc)
+    m_host, _ = build_bricks(cl)
+    for k in ("brick_lower", "brick_level", "brick_dims", "brick_offset", "scalars"):
+        assert np.array_equal(getattr(m_dev, k), getattr(m_host, k)), k
+    with open(path, "ab") as fh:
+        fh.write(b"x")
+    with pytest.raises(xio.ExaCellsError):
+        xio.load_cells_device(path)

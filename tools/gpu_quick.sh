@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_service.py -q -m gpu -x --timeout 900 > gpurun_out/pt_svc1.log 2>&1; tail -25 gpurun_out/pt_svc1.log
+timeout 1200 python -m pytest tests/test_gpu_synth.py -q -m gpu -x --timeout 900 > gpurun_out/pt_ld1.log 2>&1; tail -15 gpurun_out/pt_ld1.log
