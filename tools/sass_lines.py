@@ -25,7 +25,13 @@ def sass_csv(rep, kfilter=None):
     out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
-    return hdr, rows[2:]
+    body = []
+    for r in rows[2:]:  # first kernel block only
+        if r and r[0] == "Kernel Name":
+            break
+        if r and r[0].startswith("0x"):
+            body.append(r)
+    return hdr, body
 
 
 def line_map(cubin, prefix):
