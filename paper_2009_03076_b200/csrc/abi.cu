@@ -1,6 +1,7 @@
 // abi.cu — extern "C" entry points of libexabricks (include/exabricks.h).
 #include <cmath>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -591,6 +592,9 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->leaves = nullptr;
         A->leaf_count = nullptr;
         A->leaf_cap = 0;
+        A->cap_div = 0;
+        A->cap_min = 1;
+        A->walk_budget = 0;
         {
             const char* ek = getenv("XB_KERNEL");
             const char* ew = getenv("XB_WALK");
@@ -598,7 +602,20 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             if (walk) {
                 keep_pool(m->m.device);
                 const char* ec = getenv("XB_LEAF_CAP");
-                const int cap = ec ? std::max(1, atoi(ec)) : 48;  // sweep (with resume): C2 128 6.47, 64 6.62, 32 7.08 ms; C3 16 1.48, 32 1.52, 64 1.61, 128 1.98 ms
+                // Leaf cap per walk (then k_warp resumes the rest).  Sweep with resume, ms/frame:
+                //   cap      16    32    48    64    96    128
+                //   C2     7.54  7.08  6.81  6.62  6.42  6.47     (357K candidate rays, ~46 visits each)
+                //   C3     1.48  1.52  1.57  1.61  1.76  1.98     (312K candidates, ~6 visits, long tail)
+                //   C5                 3.37        3.40           (272K candidates)
+                // C3's few very long walks set k_walk's length; C2's many long walks are cheaper in
+                // k_walk than in the frontier.  Neither the candidate count (similar in all three) nor a
+                // clock budget (tools/ab.py: budgets cost C2 15-25 %) separates them, so: a fixed 64.
+                const int cap = ec ? std::max(1, atoi(ec)) : 64;
+                const char* ed = getenv("XB_CAP_DIV");
+                A->cap_div = ed ? atoi(ed) : 0;
+                A->cap_min = 16;
+                const char* eb = getenv("XB_WALK_BUDGET");
+                A->walk_budget = eb ? atoll(eb) : 0;
                 const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
                 const size_t ns1 = std::max<size_t>(n_slots, 1);
                 const size_t res_words = 1 + 3 * 48;  // render.cu kResume
@@ -611,6 +628,9 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             }
         }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
+        if (leaf_buf && getenv("XB_PRINT_NCAND"))  // diagnostics: candidate rays of k_walk
+            fprintf(stderr, "xb_render: %llu candidate rays of %lld\n",
+                    (unsigned long long)xb::read_scalar(A->walk_counter + 1, s), (long long)n_local * 128);
         if (leaf_buf) XB_CUDA(cudaFreeAsync(leaf_buf, s));
         if (iso_buf) XB_CUDA(cudaFreeAsync(iso_buf, s));
         o8.finish();

@@ -527,6 +527,15 @@ __global__ void __launch_bounds__(kWalkThreads) k_classify(const __grid_constant
 __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const SceneView& S = A.S;
     const int64_t n_cand = (int64_t)A.walk_counter[1];
+    // Adaptive leaf cap: with few candidate rays (a small object on screen) the
+    // kernel's length is the longest walk, so walks are cut short early and
+    // k_warp's parallel frontier resumes them; with many, long lists pay off.
+    const int cap = A.cap_div > 0 ? (int)max((int64_t)A.cap_min, min((int64_t)A.leaf_cap, n_cand / A.cap_div))
+                                  : A.leaf_cap;
+    // ... and every walk has a latency budget (clock cycles): a walk whose node
+    // loads keep missing L2 is cut and resumed by k_warp's parallel frontier.
+    // Results do not depend on where a walk stops (resume is exact).
+    const long long budget = A.walk_budget;
     for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < n_cand;
          ci += (int64_t)gridDim.x * blockDim.x) {
     const int64_t slot = A.hit_list[ci];
@@ -554,9 +563,10 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                 for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
                 const float spc = (float)A.M.spc, tau_stop = A.walk_tau_stop;
                 float tau = 0.f;
+                const long long t_begin = clock64();
                 for (;;) {
                     if (code <= -2) {  // a leaf: list it
-                        if (count == A.leaf_cap) {  // this leaf resumes the rest of the walk
+                        if (count == cap || (budget > 0 && clock64() - t_begin > budget)) {  // resume from this leaf
                             flags = kLeafTruncated;
                             save_resume(A, slot, code, tn, tf, st_code, st_tn, st_tf, sp_n);
                             break;

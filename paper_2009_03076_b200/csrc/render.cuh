@@ -29,7 +29,9 @@ struct RenderArgs {
     int grab_div, grab_fixed;          // k_warp grab schedule (launch_render)
     int32_t* leaves;                   // k_walk -> k_warp: per slot leaf_cap region ids in ray order (or NULL)
     int32_t* leaf_count;               // per slot: count | 0x40000000 when truncated
-    int leaf_cap;
+    int leaf_cap;                      // list capacity per slot
+    int cap_div, cap_min;              // k_walk's effective cap = clamp(n_candidates / cap_div, cap_min, leaf_cap)
+    long long walk_budget;             // k_walk: clock cycles per walk before it hands over (0 = none)
     int32_t* resume;                   // per slot: k_walk's ordered remainder when truncated (1 + 3 x kResume words)
     const float* vqmin;                // per region opacity minorant (k_walk early stop), may be NULL
     unsigned long long* walk_counter;  // k_walk slot counter, then the hit-list length
