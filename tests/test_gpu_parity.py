@@ -483,3 +483,44 @@ def test_acceptance_million_cells_vs_oracle(xb):
         u8r, f64r, cntr, str_ = render_frame_float(scene, cam, tf, params)
         assert np.array_equal(cntr, cnt) and np.array_equal(u8r, u8)
         assert tuple(str_[:2]) == tuple(stats[:2])
+
+
+# ---------------------------------------------------------------- screen tiles (multi-GPU layout on one GPU)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_tiled_ranks_reassemble_the_frame(xb, world):
+    """Each rank's packed tiles (global pixel index in the jitter hash), rendered
+    here one rank after another, unpack (device `xb_unpack_tiles` and the host
+    mirror) to exactly the single-GPU frame; counters add up."""
+    import torch
+
+    from paper_2009_03076_b200 import _native as N
+    from paper_2009_03076_b200.accel import TransferFunction
+    from paper_2009_03076_b200.orbit import orbit_cameras
+    from paper_2009_03076_b200.parallel import TILE_PX, tiles_of_rank, tiles_per_rank, unpack_host
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame, render_native
+
+    model, _, regions = _build("gauss_aniso")
+    lo, hi = model.value_range(0)
+    tf = TransferFunction.grayscale((lo, hi), max_alpha=0.6)
+    scene = build_scene(model, regions, tf)
+    W, H = 100, 52  # partial tiles on both edges
+    cam = orbit_cameras(regions.bounds, 3, W, H)[1]
+    p = MarchParams(seed=9, gradient_mode="analytic")
+    full = render_frame(scene, cam, tf, p)
+    slots = tiles_per_rank(W, H, world)
+    gathered = torch.zeros((world * slots * TILE_PX, 4), dtype=torch.uint8, device="cuda")
+    bufs, tot = [], np.zeros(2, np.int64)
+    for r in range(world):
+        part = gathered[r * slots * TILE_PX:(r + 1) * slots * TILE_PX]
+        if tiles_of_rank(W, H, r, world):
+            st = render_native(scene, cam, tf, p, part.data_ptr(), tile_rank=r, tile_world=world)
+            tot += st[:2]
+        bufs.append(part.cpu().numpy())
+    assert np.array_equal(unpack_host(bufs, W, H, world), full.rgba)
+    img = torch.empty((H, W, 4), dtype=torch.uint8, device="cuda")
+    N.check(N.lib().xb_unpack_tiles(N.ptr(gathered.data_ptr()), slots, world, W, H, N.ptr(img.data_ptr()), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(img.cpu().numpy(), full.rgba)
+    assert tuple(tot) == (full.stats.regions, full.stats.samples)

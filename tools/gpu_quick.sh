@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for c in c2 c3 c5; do XB_PRINT_NCAND=1 timeout 300 python tools/ab.py $c warp 1 2>&1 | grep "candidate" | tail -1; done
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -m gpu -x --timeout 900 -k "tiled" > gpurun_out/pt_tiled.log 2>&1; tail -15 gpurun_out/pt_tiled.log
