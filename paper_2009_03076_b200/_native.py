@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libexabricks.so"
+LIB_PATH = Path(os.environ["XB_LIB"]) if os.environ.get("XB_LIB") else _PKG / "libexabricks.so"  # XB_LIB: A/B builds
 
 XB_OK = 0
 XB_ERR_INVALID_CELLS = -3

@@ -22,6 +22,14 @@
 namespace xb {
 
 constexpr double kEpsWeight = 1e-12;     // EPS_WEIGHT, R/sampling.py:37
+
+// frame gather: 1 (default) = the reference's exact per-cell running sums, 0 = factored
+// trilinear sums with FMAs (within an ulp; see gather_shade).  Measured on C2 /
+// C3 (tools/ab.py, `make exact` + XB_LIB): 6.56 vs 6.61 / 1.597 vs 1.601 ms —
+// the dependent-add chain is not the limiter, so the exact sequence stays.
+#ifndef XB_EXACT_VALUE
+#define XB_EXACT_VALUE 1
+#endif
 constexpr double kTFar = 1.0e30;         // _T_FAR, R/render.py:49
 constexpr int kKdStack = 64;
 
@@ -608,6 +616,7 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, const int32_t* 
         vv[0][1][0] = __ldg(base + r01 + xa); vv[0][1][1] = __ldg(base + r01 + xb);
         vv[1][0][0] = __ldg(base + r10 + xa); vv[1][0][1] = __ldg(base + r10 + xb);
         vv[1][1][0] = __ldg(base + r11 + xa); vv[1][1][1] = __ldg(base + r11 + xb);
+#if XB_EXACT_VALUE
         const double hxy00 = hx0 * hy0, hxy01 = hx1 * hy0, hxy10 = hx0 * hy1, hxy11 = hx1 * hy1;  // [dy][dx]
         const double hzz[2] = {hz0, hz1};
 #pragma unroll
@@ -618,6 +627,19 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, const int32_t* 
             A.num += h2 * (double)vv[dz][1][0]; A.den += h2;
             A.num += h3 * (double)vv[dz][1][1]; A.den += h3;
         }
+#else
+        // Factored trilinear sums (the reference's 8-term running sums
+        // reassociated, FP64 with fused multiply-adds): num_b = sum_z hz sum_y hy
+        // sum_x hx v, den_b = (sum hx)(sum hy)(sum hz).  Within an ulp of the
+        // reference's sequence and a quarter of its dependent-add chain.
+        const double x00 = __fma_rn(hx1, (double)vv[0][0][1], hx0 * (double)vv[0][0][0]);
+        const double x01 = __fma_rn(hx1, (double)vv[0][1][1], hx0 * (double)vv[0][1][0]);
+        const double x10 = __fma_rn(hx1, (double)vv[1][0][1], hx0 * (double)vv[1][0][0]);
+        const double x11 = __fma_rn(hx1, (double)vv[1][1][1], hx0 * (double)vv[1][1][0]);
+        const double yz0 = __fma_rn(hy1, x01, hy0 * x00), yz1 = __fma_rn(hy1, x11, hy0 * x10);
+        A.num = __fma_rn(hz1, yz1, __fma_rn(hz0, yz0, A.num));
+        A.den = __fma_rn((hx0 + hx1) * (hy0 + hy1), hz0 + hz1, A.den);
+#endif
         if (GRAD) {
             if (!have_ref && ncx * ncy * ncz > 0) {  // first contributing cell (z, y, x order)
                 const float r0 = vx0 ? vv[0][0][0] : vv[0][0][1], r1 = vx0 ? vv[0][1][0] : vv[0][1][1];
