@@ -564,124 +564,144 @@ struct FastAccum {
     int n_nz;
 };
 
+// Running state of the frame gather of one sample (value sums in the
+// reference's exact FP64 sequence; FP32 shading-gradient partials).
+struct ShadeAcc {
+    double num, den;
+    float fden, gnum, dn0, dn1, dn2, dd0, dd1, dd2, v0;
+    int n_nz;
+    bool have_ref;
+    __device__ __forceinline__ void clear() {
+        num = den = 0.0;
+        fden = gnum = dn0 = dn1 = dn2 = dd0 = dd1 = dd2 = v0 = 0.f;
+        n_nz = 0;
+        have_ref = false;
+    }
+    // quotient-rule numerator of the analytic gradient (direction only, see FastAccum)
+    __device__ __forceinline__ void gradient(float g[3]) const {
+        g[0] = dn0 * fden - gnum * dd0;
+        g[1] = dn1 * fden - gnum * dd1;
+        g[2] = dn2 * fden - gnum * dd2;
+    }
+};
+
+// one brick of the frame gather: adds brick b's window cells to A
+template <bool GRAD>
+__device__ __forceinline__ void brick_step(const SceneView& S, int b, double px, double py, double pz, ShadeAcc& A) {
+    const int4 ba = __ldg(S.brick_a + b);
+    const uint32_t bm = __ldg(S.brick_m + b);
+    const int lev = bm & 31;
+    const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
+    const double w = pow2(lev), iw_d = pow2(-lev);
+    const double fx = floor((px - (double)ba.x) * iw_d - 0.5);
+    const double fy = floor((py - (double)ba.y) * iw_d - 0.5);
+    const double fz = floor((pz - (double)ba.z) * iw_d - 0.5);
+    if (!(fx >= -1.0 && fx < (double)nx && fy >= -1.0 && fy < (double)ny && fz >= -1.0 && fz < (double)nz)) return;
+    const int x0 = (int)fx, y0 = (int)fy, z0 = (int)fz;
+    const double half = 0.5 * w;
+    const double cx0 = (double)(ba.x + x0 * (1 << lev)) + half, cx1 = cx0 + w;
+    const double cy0 = (double)(ba.y + y0 * (1 << lev)) + half, cy1 = cy0 + w;
+    const double cz0 = (double)(ba.z + z0 * (1 << lev)) + half, cz1 = cz0 + w;
+    const double ex0 = cx0 - px, ex1 = cx1 - px, ey0 = cy0 - py, ey1 = cy1 - py, ez0 = cz0 - pz, ez1 = cz1 - pz;
+    double hx0 = 1.0 - fabs(ex0) * iw_d, hx1 = 1.0 - fabs(ex1) * iw_d;
+    double hy0 = 1.0 - fabs(ey0) * iw_d, hy1 = 1.0 - fabs(ey1) * iw_d;
+    double hz0 = 1.0 - fabs(ez0) * iw_d, hz1 = 1.0 - fabs(ez1) * iw_d;
+    // A window cell contributes iff its three axis slots are valid (inside
+    // the brick, hat > 0).  Zeroing the hat of an invalid slot turns every
+    // skipped term into +0 (h) and +-0 (h*v), which leave the running sums
+    // bit-identical, so the 8 cells run branch-free; loads use clamped,
+    // in-brick indices.
+    const bool vx0 = x0 >= 0 && hx0 > 0.0, vx1 = x0 + 1 < nx && hx1 > 0.0;
+    const bool vy0 = y0 >= 0 && hy0 > 0.0, vy1 = y0 + 1 < ny && hy1 > 0.0;
+    const bool vz0 = z0 >= 0 && hz0 > 0.0, vz1 = z0 + 1 < nz && hz1 > 0.0;
+    hx0 = vx0 ? hx0 : 0.0; hx1 = vx1 ? hx1 : 0.0;
+    hy0 = vy0 ? hy0 : 0.0; hy1 = vy1 ? hy1 : 0.0;
+    hz0 = vz0 ? hz0 : 0.0; hz1 = vz1 ? hz1 : 0.0;
+    const int ncx = (int)vx0 + (int)vx1, ncy = (int)vy0 + (int)vy1, ncz = (int)vz0 + (int)vz1;
+    A.n_nz += ncx * ncy * ncz;
+    const int xa = max(x0, 0), xb = min(x0 + 1, nx - 1);
+    const int ya = max(y0, 0), yb = min(y0 + 1, ny - 1);
+    const int za = max(z0, 0), zb = min(z0 + 1, nz - 1);
+    const float* __restrict__ base = S.vals + (uint32_t)ba.w;
+    const int r00 = nx * (ya + ny * za), r01 = nx * (yb + ny * za), r10 = nx * (ya + ny * zb),
+              r11 = nx * (yb + ny * zb);
+    float vv[2][2][2];  // [dz][dy][dx]
+    vv[0][0][0] = __ldg(base + r00 + xa); vv[0][0][1] = __ldg(base + r00 + xb);
+    vv[0][1][0] = __ldg(base + r01 + xa); vv[0][1][1] = __ldg(base + r01 + xb);
+    vv[1][0][0] = __ldg(base + r10 + xa); vv[1][0][1] = __ldg(base + r10 + xb);
+    vv[1][1][0] = __ldg(base + r11 + xa); vv[1][1][1] = __ldg(base + r11 + xb);
+#if XB_EXACT_VALUE
+    const double hxy00 = hx0 * hy0, hxy01 = hx1 * hy0, hxy10 = hx0 * hy1, hxy11 = hx1 * hy1;  // [dy][dx]
+    const double hzz[2] = {hz0, hz1};
+#pragma unroll
+    for (int dz = 0; dz < 2; dz++) {  // z, y, x ascending: the reference's order
+        const double h0 = hxy00 * hzz[dz], h1 = hxy01 * hzz[dz], h2 = hxy10 * hzz[dz], h3 = hxy11 * hzz[dz];
+        A.num += h0 * (double)vv[dz][0][0]; A.den += h0;
+        A.num += h1 * (double)vv[dz][0][1]; A.den += h1;
+        A.num += h2 * (double)vv[dz][1][0]; A.den += h2;
+        A.num += h3 * (double)vv[dz][1][1]; A.den += h3;
+    }
+#else
+    // Factored trilinear sums (the reference's 8-term running sums
+    // reassociated, FP64 with fused multiply-adds): num_b = sum_z hz sum_y hy
+    // sum_x hx v, den_b = (sum hx)(sum hy)(sum hz).  Within an ulp of the
+    // reference's sequence and a quarter of its dependent-add chain.
+    const double x00 = __fma_rn(hx1, (double)vv[0][0][1], hx0 * (double)vv[0][0][0]);
+    const double x01 = __fma_rn(hx1, (double)vv[0][1][1], hx0 * (double)vv[0][1][0]);
+    const double x10 = __fma_rn(hx1, (double)vv[1][0][1], hx0 * (double)vv[1][0][0]);
+    const double x11 = __fma_rn(hx1, (double)vv[1][1][1], hx0 * (double)vv[1][1][0]);
+    const double yz0 = __fma_rn(hy1, x01, hy0 * x00), yz1 = __fma_rn(hy1, x11, hy0 * x10);
+    A.num = __fma_rn(hz1, yz1, __fma_rn(hz0, yz0, A.num));
+    A.den = __fma_rn((hx0 + hx1) * (hy0 + hy1), hz0 + hz1, A.den);
+#endif
+    if (GRAD) {
+        if (!A.have_ref && ncx * ncy * ncz > 0) {  // first contributing cell (z, y, x order)
+            const float r0 = vx0 ? vv[0][0][0] : vv[0][0][1], r1 = vx0 ? vv[0][1][0] : vv[0][1][1];
+            const float r2 = vx0 ? vv[1][0][0] : vv[1][0][1], r3 = vx0 ? vv[1][1][0] : vv[1][1][1];
+            const float p0 = vy0 ? r0 : r1, p1 = vy0 ? r2 : r3;
+            A.v0 = vz0 ? p0 : p1;  // select chain: no local-memory indexing
+            A.have_ref = true;
+        }
+        const float fw = (float)iw_d;
+        const float ax0 = (float)hx0, ax1 = (float)hx1, ay0 = (float)hy0, ay1 = (float)hy1, az0 = (float)hz0,
+                    az1 = (float)hz1;
+        const float sx0 = vx0 ? (ex0 > 0.0 ? fw : -fw) : 0.f, sx1 = vx1 ? (ex1 > 0.0 ? fw : -fw) : 0.f;
+        const float sy0 = vy0 ? (ey0 > 0.0 ? fw : -fw) : 0.f, sy1 = vy1 ? (ey1 > 0.0 ? fw : -fw) : 0.f;
+        const float sz0 = vz0 ? (ez0 > 0.0 ? fw : -fw) : 0.f, sz1 = vz1 ? (ez1 > 0.0 ? fw : -fw) : 0.f;
+        float C[2], D[2], E[2];
+#pragma unroll
+        for (int dz = 0; dz < 2; dz++) {
+            const float u00 = vv[dz][0][0] - A.v0, u01 = vv[dz][0][1] - A.v0;
+            const float u10 = vv[dz][1][0] - A.v0, u11 = vv[dz][1][1] - A.v0;
+            const float A0 = fmaf(ax1, u01, ax0 * u00), A1 = fmaf(ax1, u11, ax0 * u10);  // x-hat reductions
+            const float B0 = fmaf(sx1, u01, sx0 * u00), B1 = fmaf(sx1, u11, sx0 * u10);  // x-slope reductions
+            C[dz] = fmaf(ay1, A1, ay0 * A0);  // sum hx hy u
+            D[dz] = fmaf(ay1, B1, ay0 * B0);  // sum sx hy u
+            E[dz] = fmaf(sy1, A1, sy0 * A0);  // sum hx sy u
+        }
+        A.gnum = fmaf(az1, C[1], fmaf(az0, C[0], A.gnum));
+        A.dn0 = fmaf(az1, D[1], fmaf(az0, D[0], A.dn0));
+        A.dn1 = fmaf(az1, E[1], fmaf(az0, E[0], A.dn1));
+        A.dn2 = fmaf(sz1, C[1], fmaf(sz0, C[0], A.dn2));
+        const float Hx = ax0 + ax1, Hy = ay0 + ay1, Hz = az0 + az1;
+        const float Sx = sx0 + sx1, Sy = sy0 + sy1, Sz = sz0 + sz1;
+        A.fden = fmaf(Hx * Hy, Hz, A.fden);
+        A.dd0 = fmaf(Sx * Hy, Hz, A.dd0);
+        A.dd1 = fmaf(Hx * Sy, Hz, A.dd1);
+        A.dd2 = fmaf(Hx * Hy, Sz, A.dd2);
+    }
+}
+
 template <bool GRAD>
 __device__ __forceinline__ void gather_shade(const SceneView& S, const int32_t* __restrict__ ids, int nids, double px,
-                                             double py, double pz, FastAccum& A) {
-    A.num = 0.0;
-    A.den = 0.0;
-    A.n_nz = 0;
-    float fden = 0.f, gnum = 0.f, dn0 = 0.f, dn1 = 0.f, dn2 = 0.f, dd0 = 0.f, dd1 = 0.f, dd2 = 0.f, v0 = 0.f;
-    bool have_ref = false;
-    for (int t = 0; t < nids; t++) {
-        const int b = __ldg(ids + t);
-        const int4 ba = __ldg(S.brick_a + b);
-        const uint32_t bm = __ldg(S.brick_m + b);
-        const int lev = bm & 31;
-        const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
-        const double w = pow2(lev), iw_d = pow2(-lev);
-        const double fx = floor((px - (double)ba.x) * iw_d - 0.5);
-        const double fy = floor((py - (double)ba.y) * iw_d - 0.5);
-        const double fz = floor((pz - (double)ba.z) * iw_d - 0.5);
-        if (!(fx >= -1.0 && fx < (double)nx && fy >= -1.0 && fy < (double)ny && fz >= -1.0 && fz < (double)nz)) continue;
-        const int x0 = (int)fx, y0 = (int)fy, z0 = (int)fz;
-        const double half = 0.5 * w;
-        const double cx0 = (double)(ba.x + x0 * (1 << lev)) + half, cx1 = cx0 + w;
-        const double cy0 = (double)(ba.y + y0 * (1 << lev)) + half, cy1 = cy0 + w;
-        const double cz0 = (double)(ba.z + z0 * (1 << lev)) + half, cz1 = cz0 + w;
-        const double ex0 = cx0 - px, ex1 = cx1 - px, ey0 = cy0 - py, ey1 = cy1 - py, ez0 = cz0 - pz, ez1 = cz1 - pz;
-        double hx0 = 1.0 - fabs(ex0) * iw_d, hx1 = 1.0 - fabs(ex1) * iw_d;
-        double hy0 = 1.0 - fabs(ey0) * iw_d, hy1 = 1.0 - fabs(ey1) * iw_d;
-        double hz0 = 1.0 - fabs(ez0) * iw_d, hz1 = 1.0 - fabs(ez1) * iw_d;
-        // A window cell contributes iff its three axis slots are valid (inside
-        // the brick, hat > 0).  Zeroing the hat of an invalid slot turns every
-        // skipped term into +0 (h) and +-0 (h*v), which leave the running sums
-        // bit-identical, so the 8 cells run branch-free; loads use clamped,
-        // in-brick indices.
-        const bool vx0 = x0 >= 0 && hx0 > 0.0, vx1 = x0 + 1 < nx && hx1 > 0.0;
-        const bool vy0 = y0 >= 0 && hy0 > 0.0, vy1 = y0 + 1 < ny && hy1 > 0.0;
-        const bool vz0 = z0 >= 0 && hz0 > 0.0, vz1 = z0 + 1 < nz && hz1 > 0.0;
-        hx0 = vx0 ? hx0 : 0.0; hx1 = vx1 ? hx1 : 0.0;
-        hy0 = vy0 ? hy0 : 0.0; hy1 = vy1 ? hy1 : 0.0;
-        hz0 = vz0 ? hz0 : 0.0; hz1 = vz1 ? hz1 : 0.0;
-        const int ncx = (int)vx0 + (int)vx1, ncy = (int)vy0 + (int)vy1, ncz = (int)vz0 + (int)vz1;
-        A.n_nz += ncx * ncy * ncz;
-        const int xa = max(x0, 0), xb = min(x0 + 1, nx - 1);
-        const int ya = max(y0, 0), yb = min(y0 + 1, ny - 1);
-        const int za = max(z0, 0), zb = min(z0 + 1, nz - 1);
-        const float* __restrict__ base = S.vals + (uint32_t)ba.w;
-        const int r00 = nx * (ya + ny * za), r01 = nx * (yb + ny * za), r10 = nx * (ya + ny * zb),
-                  r11 = nx * (yb + ny * zb);
-        float vv[2][2][2];  // [dz][dy][dx]
-        vv[0][0][0] = __ldg(base + r00 + xa); vv[0][0][1] = __ldg(base + r00 + xb);
-        vv[0][1][0] = __ldg(base + r01 + xa); vv[0][1][1] = __ldg(base + r01 + xb);
-        vv[1][0][0] = __ldg(base + r10 + xa); vv[1][0][1] = __ldg(base + r10 + xb);
-        vv[1][1][0] = __ldg(base + r11 + xa); vv[1][1][1] = __ldg(base + r11 + xb);
-#if XB_EXACT_VALUE
-        const double hxy00 = hx0 * hy0, hxy01 = hx1 * hy0, hxy10 = hx0 * hy1, hxy11 = hx1 * hy1;  // [dy][dx]
-        const double hzz[2] = {hz0, hz1};
-#pragma unroll
-        for (int dz = 0; dz < 2; dz++) {  // z, y, x ascending: the reference's order
-            const double h0 = hxy00 * hzz[dz], h1 = hxy01 * hzz[dz], h2 = hxy10 * hzz[dz], h3 = hxy11 * hzz[dz];
-            A.num += h0 * (double)vv[dz][0][0]; A.den += h0;
-            A.num += h1 * (double)vv[dz][0][1]; A.den += h1;
-            A.num += h2 * (double)vv[dz][1][0]; A.den += h2;
-            A.num += h3 * (double)vv[dz][1][1]; A.den += h3;
-        }
-#else
-        // Factored trilinear sums (the reference's 8-term running sums
-        // reassociated, FP64 with fused multiply-adds): num_b = sum_z hz sum_y hy
-        // sum_x hx v, den_b = (sum hx)(sum hy)(sum hz).  Within an ulp of the
-        // reference's sequence and a quarter of its dependent-add chain.
-        const double x00 = __fma_rn(hx1, (double)vv[0][0][1], hx0 * (double)vv[0][0][0]);
-        const double x01 = __fma_rn(hx1, (double)vv[0][1][1], hx0 * (double)vv[0][1][0]);
-        const double x10 = __fma_rn(hx1, (double)vv[1][0][1], hx0 * (double)vv[1][0][0]);
-        const double x11 = __fma_rn(hx1, (double)vv[1][1][1], hx0 * (double)vv[1][1][0]);
-        const double yz0 = __fma_rn(hy1, x01, hy0 * x00), yz1 = __fma_rn(hy1, x11, hy0 * x10);
-        A.num = __fma_rn(hz1, yz1, __fma_rn(hz0, yz0, A.num));
-        A.den = __fma_rn((hx0 + hx1) * (hy0 + hy1), hz0 + hz1, A.den);
-#endif
-        if (GRAD) {
-            if (!have_ref && ncx * ncy * ncz > 0) {  // first contributing cell (z, y, x order)
-                const float r0 = vx0 ? vv[0][0][0] : vv[0][0][1], r1 = vx0 ? vv[0][1][0] : vv[0][1][1];
-                const float r2 = vx0 ? vv[1][0][0] : vv[1][0][1], r3 = vx0 ? vv[1][1][0] : vv[1][1][1];
-                const float p0 = vy0 ? r0 : r1, p1 = vy0 ? r2 : r3;
-                v0 = vz0 ? p0 : p1;  // select chain: no local-memory indexing
-                have_ref = true;
-            }
-            const float fw = (float)iw_d;
-            const float ax0 = (float)hx0, ax1 = (float)hx1, ay0 = (float)hy0, ay1 = (float)hy1, az0 = (float)hz0,
-                        az1 = (float)hz1;
-            const float sx0 = vx0 ? (ex0 > 0.0 ? fw : -fw) : 0.f, sx1 = vx1 ? (ex1 > 0.0 ? fw : -fw) : 0.f;
-            const float sy0 = vy0 ? (ey0 > 0.0 ? fw : -fw) : 0.f, sy1 = vy1 ? (ey1 > 0.0 ? fw : -fw) : 0.f;
-            const float sz0 = vz0 ? (ez0 > 0.0 ? fw : -fw) : 0.f, sz1 = vz1 ? (ez1 > 0.0 ? fw : -fw) : 0.f;
-            float C[2], D[2], E[2];
-#pragma unroll
-            for (int dz = 0; dz < 2; dz++) {
-                const float u00 = vv[dz][0][0] - v0, u01 = vv[dz][0][1] - v0;
-                const float u10 = vv[dz][1][0] - v0, u11 = vv[dz][1][1] - v0;
-                const float A0 = fmaf(ax1, u01, ax0 * u00), A1 = fmaf(ax1, u11, ax0 * u10);  // x-hat reductions
-                const float B0 = fmaf(sx1, u01, sx0 * u00), B1 = fmaf(sx1, u11, sx0 * u10);  // x-slope reductions
-                C[dz] = fmaf(ay1, A1, ay0 * A0);  // sum hx hy u
-                D[dz] = fmaf(ay1, B1, ay0 * B0);  // sum sx hy u
-                E[dz] = fmaf(sy1, A1, sy0 * A0);  // sum hx sy u
-            }
-            gnum = fmaf(az1, C[1], fmaf(az0, C[0], gnum));
-            dn0 = fmaf(az1, D[1], fmaf(az0, D[0], dn0));
-            dn1 = fmaf(az1, E[1], fmaf(az0, E[0], dn1));
-            dn2 = fmaf(sz1, C[1], fmaf(sz0, C[0], dn2));
-            const float Hx = ax0 + ax1, Hy = ay0 + ay1, Hz = az0 + az1;
-            const float Sx = sx0 + sx1, Sy = sy0 + sy1, Sz = sz0 + sz1;
-            fden = fmaf(Hx * Hy, Hz, fden);
-            dd0 = fmaf(Sx * Hy, Hz, dd0);
-            dd1 = fmaf(Hx * Sy, Hz, dd1);
-            dd2 = fmaf(Hx * Hy, Sz, dd2);
-        }
-    }
-    if (GRAD) {
-        A.g[0] = dn0 * fden - gnum * dd0;
-        A.g[1] = dn1 * fden - gnum * dd1;
-        A.g[2] = dn2 * fden - gnum * dd2;
-    }
+                                             double py, double pz, FastAccum& F) {
+    ShadeAcc A;
+    A.clear();
+    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, __ldg(ids + t), px, py, pz, A);
+    F.num = A.num;
+    F.den = A.den;
+    F.n_nz = A.n_nz;
+    if (GRAD) A.gradient(F.g);
 }
 
 // ---------------------------------------------------------------------------
