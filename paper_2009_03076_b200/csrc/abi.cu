@@ -591,6 +591,7 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         int32_t* leaf_buf = nullptr;
         A->leaves = nullptr;
         A->leaf_count = nullptr;
+        A->short_list = nullptr;
         A->leaf_cap = 0;
         A->cap_div = 0;
         A->cap_min = 1;
@@ -619,18 +620,36 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                 const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
                 const size_t ns1 = std::max<size_t>(n_slots, 1);
                 const size_t res_words = 1 + 3 * 48;  // render.cu kResume
-                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 2 + res_words) * sizeof(int32_t), s));
+                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 3 + res_words) * sizeof(int32_t), s));
                 A->leaf_count = leaf_buf;
                 A->hit_list = leaf_buf + ns1;
-                A->resume = leaf_buf + 2 * ns1;
-                A->leaves = leaf_buf + (2 + res_words) * ns1;
+                // k_short for rays with <= 8 leaves and <= 24 estimated samples: off by default
+                // (tools/ab.py, ms: C3 1.569 vs 1.621, C2 6.78 vs 6.68, C5 3.66 vs 3.39 — one thread
+                // per ray only pays when short rays are plentiful); XB_SHORT=1 enables it.
+                const char* esh = getenv("XB_SHORT");
+                A->short_list = (esh && esh[0] == '1') ? leaf_buf + 2 * ns1 : nullptr;
+                A->resume = leaf_buf + 3 * ns1;
+                A->leaves = leaf_buf + (3 + res_words) * ns1;
                 A->leaf_cap = cap;
             }
         }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
-        if (leaf_buf && getenv("XB_PRINT_NCAND"))  // diagnostics: candidate rays of k_walk
-            fprintf(stderr, "xb_render: %llu candidate rays of %lld\n",
-                    (unsigned long long)xb::read_scalar(A->walk_counter + 1, s), (long long)n_local * 128);
+        if (leaf_buf && getenv("XB_PRINT_NCAND")) {  // diagnostics: candidate rays of k_walk + leaf histogram
+            const size_t ns = (size_t)n_local * 128;
+            std::vector<int32_t> lc(ns);
+            XB_CUDA(cudaMemcpyAsync(lc.data(), A->leaf_count, ns * 4, cudaMemcpyDeviceToHost, s));
+            XB_CUDA(cudaStreamSynchronize(s));
+            long long h[9] = {0};
+            for (int32_t v : lc) {
+                if (v & 0x40000000) { h[8]++; continue; }
+                const int c = v & 0x3fffffff;
+                h[c == 0 ? 0 : c <= 2 ? 1 : c <= 4 ? 2 : c <= 8 ? 3 : c <= 16 ? 4 : c <= 32 ? 5 : c <= 64 ? 6 : 7]++;
+            }
+            fprintf(stderr, "xb_render: %llu candidates; leaves 0:%lld 1-2:%lld 3-4:%lld 5-8:%lld 9-16:%lld "
+                            "17-32:%lld 33-64:%lld >64:%lld truncated:%lld\n",
+                    (unsigned long long)xb::read_scalar(A->walk_counter + 1, s), h[0], h[1], h[2], h[3], h[4],
+                    h[5], h[6], h[7], h[8]);
+        }
         if (leaf_buf) XB_CUDA(cudaFreeAsync(leaf_buf, s));
         if (iso_buf) XB_CUDA(cudaFreeAsync(iso_buf, s));
         o8.finish();

@@ -451,8 +451,10 @@ __device__ __forceinline__ void lattice(double ci, double co, double dt, double 
 
 constexpr int kWalkThreads = 128;
 constexpr int kWalkStack = 100;  // >= 3 x (Kd4 depth <= kKdStack / 2 + 1)
-constexpr int kLeafCountMask = 0x3fffffff;
+constexpr int kLeafCountMask = 0x1fffffff;
 constexpr int kLeafTruncated = 0x40000000;
+constexpr int kLeafHeavy = 0x20000000;  // > kShortSamples estimated samples (not for k_short)
+constexpr float kShortSamples = 24.f;
 constexpr int kResume = 48;  // resume entries saved per truncated walk
 
 // pixel of a ray that meets no active region: transparent, or the iso colour
@@ -562,7 +564,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                 int sg[3];
                 for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
                 const float spc = (float)A.M.spc, tau_stop = A.walk_tau_stop;
-                float tau = 0.f;
+                float tau = 0.f, est = 0.f;
                 const long long t_begin = clock64();
                 for (;;) {
                     if (code <= -2) {  // a leaf: list it
@@ -573,6 +575,8 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                         }
                         const int rid = -2 - code;
                         out[count++] = rid;
+                        if (est <= kShortSamples)  // sample estimate: interval / lattice step + 1
+                            est += (float)((tf - tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
                         if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
                             tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;
                             if (tau > tau_stop) {
@@ -655,19 +659,152 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                     tn = (double)st_tn[sp_n];
                     tf = (double)st_tf[sp_n];
                 }
+                if (est > kShortSamples) flags |= kLeafHeavy;
             }
         }
-        A.leaf_count[slot] = count | flags;  // 0: k_warp writes the empty pixel
+        A.leaf_count[slot] = count | flags;
+        if (count == 0 && !flags) write_empty_pixel(A, slot, spx.out, true);  // no active region on the ray
     }
     }
     (void)n_slots;
 }
 
-// hit rays (leaf_count != 0) -> k_warp's work list, in slot (screen-tile) order
+// hit rays (leaf_count != 0) -> k_walk's work list, in slot (screen-tile) order
 struct HasLeaves {
     const int32_t* c;
     __device__ __forceinline__ bool operator()(const int32_t i) const { return c[i] != 0; }
 };
+
+// after k_walk: short rays (complete lists of <= kShortLeaves leaves) go to
+// k_short, the rest (long or truncated) to k_warp
+constexpr int kShortLeaves = 8;
+struct IsShort {
+    const int32_t* c;
+    __device__ __forceinline__ bool operator()(const int32_t i) const {
+        const int v = c[i];
+        return v != 0 && !(v & (kLeafTruncated | kLeafHeavy)) && (v & kLeafCountMask) <= kShortLeaves;
+    }
+};
+struct IsLong {
+    const int32_t* c;
+    __device__ __forceinline__ bool operator()(const int32_t i) const {
+        const int v = c[i];
+        return (v & (kLeafTruncated | kLeafHeavy)) || (v & kLeafCountMask) > kShortLeaves;
+    }
+};
+
+// k_short: one thread per short ray (C3: 87 % of the rays that meet an active
+// region list 1-8 leaves and take a handful of samples, which would leave most
+// lanes of a warp-per-ray chunk idle).  The thread runs the reference's
+// _volume_ray loop over its leaf list verbatim (R/render.py:380-453: exact
+// restart chain, lattice, sequential front-to-back compositing, early
+// termination) with the frame kernel's reconstruction and shading.
+template <int GRAD, bool ISO, bool COUNT>
+__global__ void __launch_bounds__(kWalkThreads) k_short(const __grid_constant__ RenderArgs A, int64_t n_slots) {
+    __shared__ double s_tf[1024];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
+    __syncthreads();
+    const int64_t n_short = (int64_t)A.walk_counter[0];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    unsigned long long my_reg = 0, my_smp = 0, my_bytes = 0;
+    if (i < n_short) {
+        const SceneView& S = A.S;
+        const int64_t slot = A.short_list[i];
+        const SlotPix sp = slot_pixel(A, slot);
+        Ray r;
+        pixel_ray(A, sp.x, sp.y, r);
+        const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
+        double tmin = 0.0, tmax = kTFar;
+        clip_ray(A.M, r, tmin, tmax);
+        if (ISO) tmax = A.iso_tend[slot];
+        const int count = A.leaf_count[slot] & kLeafCountMask;
+        const int32_t* __restrict__ list = A.leaves + slot * (int64_t)A.leaf_cap;
+        double ar = 0.0, ag = 0.0, ab = 0.0, aa = 0.0;
+        int nreg = 0, nsmp = 0;
+        double t = tmin;
+        for (int li = 0; li < count && aa < A.M.early; li++) {
+            const int rid = list[li];
+            const RegionRec rr = S.rec[rid];
+            double r_in, r_out;
+            slab_h(rr.lo, rr.hi, r, r_in, r_out);
+            const double ci = r_in > t ? r_in : t, co = r_out < tmax ? r_out : tmax;
+            if (!(ci < co)) continue;  // not the reference's next hit
+            nreg++;
+            const int lev = rr.meta >> 24, nids = rr.meta & 0xffffff;
+            const int32_t* ids = S.rids + rr.ids_begin;
+            if (COUNT) my_bytes += 32 + 4 * (unsigned long long)nids;
+            const double dt = A.M.lv_dt[lev];
+            double prev = ci, k = floor(ci / dt - rho) + 1.0;
+            bool done = false;
+            while (!done) {
+                double tk = dt * (k + rho);
+                k += 1.0;
+                if (tk >= co) { tk = co; done = true; }
+                else if (tk <= prev) continue;
+                const double sl = tk - prev, mid = 0.5 * (prev + tk);
+                prev = tk;
+                nsmp++;
+                const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1], pz = r.o[2] + mid * r.d[2];
+                FastAccum F;
+                gather_shade<GRAD == 1>(S, ids, nids, px, py, pz, F);
+                if (COUNT) my_bytes += 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
+                if (F.den > kEpsWeight) {
+                    const double v = F.num / F.den;
+                    double c[4];
+                    tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_inv, v, c);
+                    if (c[3] > 0.0) {
+                        const double alpha = opacity_correct(c[3], sl * A.M.lv_is1[lev]);
+                        if (GRAD != 0) {
+                            double f;
+                            if (GRAD == 1) {
+                                f = shade_factor_f(F.g, r);
+                            } else {
+                                double g[3];
+                                int64_t ne = 0;
+                                central_gradient(S, A.M.grad_mode, px, py, pz, rid, ids, nids, v, g, &ne);
+                                f = shade_factor(g, r);
+                            }
+                            c[0] *= f; c[1] *= f; c[2] *= f;
+                        }
+                        const double w = alpha * (1.0 - aa);
+                        ar += w * c[0];
+                        ag += w * c[1];
+                        ab += w * c[2];
+                        aa += w;
+                        if (aa >= A.M.early) break;
+                    }
+                }
+            }
+            t = restart_t(co);
+            if (t >= tmax) break;
+        }
+        double acc[4] = {ar, ag, ab, aa};
+        if (ISO) {
+            const double f = A.iso_shade[slot];
+            if (f >= 0.0) {
+                const double wgt = 1.0 - acc[3];
+                acc[0] += wgt * A.M.iso_rgb[0] * f;
+                acc[1] += wgt * A.M.iso_rgb[1] * f;
+                acc[2] += wgt * A.M.iso_rgb[2] * f;
+                acc[3] = 1.0;
+            }
+        }
+        write_pixel(A, sp.out, acc, nreg, nsmp);
+        my_reg = nreg;
+        my_smp = nsmp;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        my_reg += __shfl_xor_sync(0xffffffffu, my_reg, o);
+        my_smp += __shfl_xor_sync(0xffffffffu, my_smp, o);
+        if (COUNT) my_bytes += __shfl_xor_sync(0xffffffffu, my_bytes, o);
+    }
+    if ((threadIdx.x & 31) == 0 && A.stats && (my_reg | my_smp)) {
+        atomicAdd(&A.stats[0], my_reg);
+        atomicAdd(&A.stats[1], my_smp);
+        if (COUNT) atomicAdd(&A.stats[2], my_bytes);
+    }
+    (void)n_slots;
+}
 
 template <int GRAD, bool ISO, bool COUNT, int MINB = kWarpMinBlocks>
 __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_constant__ RenderArgs A,
@@ -1367,6 +1504,24 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             // one thread per candidate (blocks past the device-side count exit at once)
             XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
                                      wargs, 0, s));
+            if (A.short_list) {  // short rays -> k_short, long ones -> k_warp (hit_list, count walk_counter[1])
+                XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.short_list, A.walk_counter, (int)n_slots,
+                                              IsShort{A.leaf_count}, s));
+                XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.hit_list, A.walk_counter + 1, (int)n_slots,
+                                              IsLong{A.leaf_count}, s));
+                using ShortFn = void (*)(RenderArgs, int64_t);
+                ShortFn sf;
+                if (g == 0) sf = iso ? (ShortFn)k_short<0, true, false> : (ShortFn)k_short<0, false, false>;
+                else if (g == 1) sf = iso ? (ShortFn)k_short<1, true, false> : (ShortFn)k_short<1, false, false>;
+                else sf = iso ? (ShortFn)k_short<2, true, false> : (ShortFn)k_short<2, false, false>;
+                if (count) {
+                    if (g == 0) sf = iso ? (ShortFn)k_short<0, true, true> : (ShortFn)k_short<0, false, true>;
+                    else if (g == 1) sf = iso ? (ShortFn)k_short<1, true, true> : (ShortFn)k_short<1, false, true>;
+                    else sf = iso ? (ShortFn)k_short<2, true, true> : (ShortFn)k_short<2, false, true>;
+                }
+                XB_CUDA(cudaLaunchKernel((const void*)sf, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
+                                         wargs, 0, s));
+            }
             XB_CUDA(cudaFreeAsync(tmp, s));
         }
         if (g == 0) fn = iso ? warp_fn<0, true>(count) : warp_fn<0, false>(count);

@@ -35,7 +35,8 @@ struct RenderArgs {
     int32_t* resume;                   // per slot: k_walk's ordered remainder when truncated (1 + 3 x kResume words)
     const float* vqmin;                // per region opacity minorant (k_walk early stop), may be NULL
     unsigned long long* walk_counter;  // k_walk slot counter, then the hit-list length
-    int32_t* hit_list;                 // slots k_walk found to meet an active region (k_warp's work)
+    int32_t* hit_list;                 // candidate rays (k_walk's work), then the long rays (k_warp's)
+    int32_t* short_list;               // rays with a complete list of <= 8 leaves (k_short's work), or NULL
     float walk_tau_stop;               // k_walk stops listing once the opacity minorant passes this depth
     int use_lbvh;                      // XB_TRAVERSAL=lbvh: per-visit LBVH closest-hit queries (tile kernel)
     LbvhView vlb, ilb;                 // LBVHs of the volume / iso active sets

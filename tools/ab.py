@@ -31,9 +31,11 @@ stream = torch.cuda.current_stream()
 def setv(v):
     """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N) | gD (guided grab divisor D)"""
     for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU",
-              "XB_TRAVERSAL", "XB_CAP_DIV", "XB_WALK_BUDGET"):
+              "XB_TRAVERSAL", "XB_CAP_DIV", "XB_WALK_BUDGET", "XB_SHORT"):
         os.environ.pop(k, None)
-    if v.startswith("bud") and v[3:].isdigit():
+    if v == "short":
+        os.environ["XB_SHORT"] = "1"
+    elif v.startswith("bud") and v[3:].isdigit():
         os.environ["XB_WALK_BUDGET"] = v[3:]
     elif v.startswith("div") and v[3:].isdigit():
         os.environ["XB_CAP_DIV"] = v[3:]
