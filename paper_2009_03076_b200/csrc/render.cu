@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                         }
                         const int rid = -2 - code;
                         out[count++] = rid;
-                        if (est <= kShortSamples)  // sample estimate: interval / lattice step + 1
+                        if (A.short_list && est <= kShortSamples)  // sample estimate: interval / step + 1
                             est += (float)((tf - tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
                         if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
                             tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;

@@ -285,6 +285,20 @@ def render_native(scene: Scene, camera: Camera, tf: TransferFunction, params: Ma
     return stats
 
 
+def _host_image(height: int, width: int) -> np.ndarray:
+    """Frame output array.  With torch present it is page-locked memory from
+    torch's caching host allocator (the D2H copy runs at full link speed and the
+    block returns to the cache when the array is freed); plain numpy otherwise."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.empty((height, width, 4), dtype=torch.uint8, pin_memory=True).numpy()
+    except Exception:  # pragma: no cover - torch missing or without CUDA
+        pass
+    return np.empty((height, width, 4), np.uint8)
+
+
 def render_frame(scene: Scene, camera: Camera, tf: TransferFunction, params: MarchParams,
                  use_celllocation: bool = False) -> Frame:
     """Render a full frame on the GPU (R/render.py:654-691).
@@ -299,7 +313,7 @@ def render_frame(scene: Scene, camera: Camera, tf: TransferFunction, params: Mar
     if use_celllocation and scene.tree is None:
         raise ValueError("cell-location sampling requires a scene built with the split tree")
     t0 = time.perf_counter()
-    out = np.empty((camera.height, camera.width, 4), np.uint8)
+    out = _host_image(camera.height, camera.width)
     stats = render_native(scene, camera, tf, params, out, use_celllocation=use_celllocation)
     ms = (time.perf_counter() - t0) * 1000.0
     return Frame(camera.width, camera.height, out, FrameStats(ms, int(stats[0]), int(stats[1])))
