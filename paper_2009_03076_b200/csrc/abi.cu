@@ -592,6 +592,7 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->leaves = nullptr;
         A->leaf_count = nullptr;
         A->short_list = nullptr;
+        A->short_min = 0;
         A->leaf_cap = 0;
         A->cap_div = 0;
         A->cap_min = 1;
@@ -623,11 +624,16 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                 XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 3 + res_words) * sizeof(int32_t), s));
                 A->leaf_count = leaf_buf;
                 A->hit_list = leaf_buf + ns1;
-                // k_short for rays with <= 8 leaves and <= 24 estimated samples: off by default
-                // (tools/ab.py, ms: C3 1.569 vs 1.621, C2 6.78 vs 6.68, C5 3.66 vs 3.39 — one thread
-                // per ray only pays when short rays are plentiful); XB_SHORT=1 enables it.
+                // k_short for rays with <= 8 leaves and <= 24 estimated samples, used only when the
+                // frame has >= 1000 x SMs of them (decided on the device).  tools/ab.py, ms, forced on
+                // vs off: C3 (270K short rays) 1.56 vs 1.61, C5 (44K) 3.70 vs 3.40, C2 (57K) 6.82 vs
+                // 6.66 — one thread per ray pays only when short rays are plentiful.  XB_SHORT=0 / 1:
+                // never / always.
                 const char* esh = getenv("XB_SHORT");
-                A->short_list = (esh && esh[0] == '1') ? leaf_buf + 2 * ns1 : nullptr;
+                int sms = 148;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->m.device);
+                A->short_list = (esh && esh[0] == '0') ? nullptr : leaf_buf + 2 * ns1;
+                A->short_min = (esh && esh[0] == '1') ? 0 : 1000ll * sms;
                 A->resume = leaf_buf + 3 * ns1;
                 A->leaves = leaf_buf + (3 + res_words) * ns1;
                 A->leaf_cap = cap;

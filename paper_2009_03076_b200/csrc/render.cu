@@ -455,6 +455,7 @@ constexpr int kLeafCountMask = 0x1fffffff;
 constexpr int kLeafTruncated = 0x40000000;
 constexpr int kLeafHeavy = 0x20000000;  // > kShortSamples estimated samples (not for k_short)
 constexpr float kShortSamples = 24.f;
+constexpr int kShortLeaves = 8;
 constexpr int kResume = 48;  // resume entries saved per truncated walk
 
 // pixel of a ray that meets no active region: transparent, or the iso colour
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                         }
                         const int rid = -2 - code;
                         out[count++] = rid;
-                        if (A.short_list && est <= kShortSamples)  // sample estimate: interval / step + 1
+                        if (A.short_list && count <= kShortLeaves && est <= kShortSamples)  // samples ~ len/dt + 1
                             est += (float)((tf - tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
                         if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
                             tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;
@@ -677,7 +678,6 @@ struct HasLeaves {
 
 // after k_walk: short rays (complete lists of <= kShortLeaves leaves) go to
 // k_short, the rest (long or truncated) to k_warp
-constexpr int kShortLeaves = 8;
 struct IsShort {
     const int32_t* c;
     __device__ __forceinline__ bool operator()(const int32_t i) const {
@@ -685,11 +685,15 @@ struct IsShort {
         return v != 0 && !(v & (kLeafTruncated | kLeafHeavy)) && (v & kLeafCountMask) <= kShortLeaves;
     }
 };
-struct IsLong {
+struct IsLong {  // long rays, plus the short ones when too few for k_short to pay (n_short < short_min)
     const int32_t* c;
+    const unsigned long long* n_short;
+    long long short_min;
     __device__ __forceinline__ bool operator()(const int32_t i) const {
         const int v = c[i];
-        return (v & (kLeafTruncated | kLeafHeavy)) || (v & kLeafCountMask) > kShortLeaves;
+        if (v == 0) return false;
+        const bool is_long = (v & (kLeafTruncated | kLeafHeavy)) || (v & kLeafCountMask) > kShortLeaves;
+        return is_long || (long long)*n_short < short_min;
     }
 };
 
@@ -702,9 +706,10 @@ struct IsLong {
 template <int GRAD, bool ISO, bool COUNT>
 __global__ void __launch_bounds__(kWalkThreads) k_short(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     __shared__ double s_tf[1024];
+    const int64_t n_short = (int64_t)A.walk_counter[0] < A.short_min ? 0 : (int64_t)A.walk_counter[0];
+    if (blockIdx.x * (int64_t)blockDim.x >= n_short) return;  // the grid covers every slot; most blocks idle
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
     __syncthreads();
-    const int64_t n_short = (int64_t)A.walk_counter[0];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     unsigned long long my_reg = 0, my_smp = 0, my_bytes = 0;
     if (i < n_short) {
@@ -1508,7 +1513,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
                 XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.short_list, A.walk_counter, (int)n_slots,
                                               IsShort{A.leaf_count}, s));
                 XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.hit_list, A.walk_counter + 1, (int)n_slots,
-                                              IsLong{A.leaf_count}, s));
+                                              IsLong{A.leaf_count, A.walk_counter, A.short_min}, s));
                 using ShortFn = void (*)(RenderArgs, int64_t);
                 ShortFn sf;
                 if (g == 0) sf = iso ? (ShortFn)k_short<0, true, false> : (ShortFn)k_short<0, false, false>;

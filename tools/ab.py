@@ -35,6 +35,8 @@ def setv(v):
         os.environ.pop(k, None)
     if v == "short":
         os.environ["XB_SHORT"] = "1"
+    elif v == "noshort":
+        os.environ["XB_SHORT"] = "0"
     elif v.startswith("bud") and v[3:].isdigit():
         os.environ["XB_WALK_BUDGET"] = v[3:]
     elif v.startswith("div") and v[3:].isdigit():

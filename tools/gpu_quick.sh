@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python bench.py --secondary '' --no-cpu-baseline > gpurun_out/bench_pin.json 2> gpurun_out/bench_pin.err; python -c "
-import json; d=json.loads(open('gpurun_out/bench_pin.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['e2e'])"
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "frames_match" > gpurun_out/pt_pin.log 2>&1; tail -1 gpurun_out/pt_pin.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -m gpu -x --timeout 900 -k "acceptance or frames_match or tiled" > gpurun_out/pt_sh4.log 2>&1; tail -1 gpurun_out/pt_sh4.log
+for c in c3 c5 c2; do timeout 300 python tools/ab.py $c warp,noshort 6 > gpurun_out/ab_sh4_$c.log 2>&1; grep median gpurun_out/ab_sh4_$c.log; done
