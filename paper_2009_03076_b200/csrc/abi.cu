@@ -593,6 +593,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->leaf_count = nullptr;
         A->short_list = nullptr;
         A->short_min = 0;
+        A->short_leaves = 8;
+        A->short_samples = 24.f;
         A->leaf_cap = 0;
         A->cap_div = 0;
         A->cap_min = 1;
@@ -634,6 +636,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->m.device);
                 A->short_list = (esh && esh[0] == '0') ? nullptr : leaf_buf + 2 * ns1;
                 A->short_min = (esh && esh[0] == '1') ? 0 : 1000ll * sms;
+                A->short_leaves = getenv("XB_SHORT_LEAVES") ? atoi(getenv("XB_SHORT_LEAVES")) : 8;
+                A->short_samples = getenv("XB_SHORT_SAMPLES") ? (float)atof(getenv("XB_SHORT_SAMPLES")) : 24.f;
                 A->resume = leaf_buf + 3 * ns1;
                 A->leaves = leaf_buf + (3 + res_words) * ns1;
                 A->leaf_cap = cap;

@@ -454,7 +454,7 @@ constexpr int kWalkStack = 100;  // >= 3 x (Kd4 depth <= kKdStack / 2 + 1)
 constexpr int kLeafCountMask = 0x1fffffff;
 constexpr int kLeafTruncated = 0x40000000;
 constexpr int kLeafHeavy = 0x20000000;  // > kShortSamples estimated samples (not for k_short)
-constexpr float kShortSamples = 24.f;
+constexpr float kShortSamples = 24.f;  // defaults of RenderArgs.short_samples / short_leaves
 constexpr int kShortLeaves = 8;
 constexpr int kResume = 48;  // resume entries saved per truncated walk
 
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                         }
                         const int rid = -2 - code;
                         out[count++] = rid;
-                        if (A.short_list && count <= kShortLeaves && est <= kShortSamples)  // samples ~ len/dt + 1
+                        if (A.short_list && count <= A.short_leaves && est <= A.short_samples)  // samples ~ len/dt + 1
                             est += (float)((tf - tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
                         if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
                             tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                     tn = (double)st_tn[sp_n];
                     tf = (double)st_tf[sp_n];
                 }
-                if (est > kShortSamples) flags |= kLeafHeavy;
+                if (est > A.short_samples) flags |= kLeafHeavy;
             }
         }
         A.leaf_count[slot] = count | flags;
@@ -680,19 +680,21 @@ struct HasLeaves {
 // k_short, the rest (long or truncated) to k_warp
 struct IsShort {
     const int32_t* c;
+    int max_leaves;
     __device__ __forceinline__ bool operator()(const int32_t i) const {
         const int v = c[i];
-        return v != 0 && !(v & (kLeafTruncated | kLeafHeavy)) && (v & kLeafCountMask) <= kShortLeaves;
+        return v != 0 && !(v & (kLeafTruncated | kLeafHeavy)) && (v & kLeafCountMask) <= max_leaves;
     }
 };
 struct IsLong {  // long rays, plus the short ones when too few for k_short to pay (n_short < short_min)
     const int32_t* c;
     const unsigned long long* n_short;
     long long short_min;
+    int max_leaves;
     __device__ __forceinline__ bool operator()(const int32_t i) const {
         const int v = c[i];
         if (v == 0) return false;
-        const bool is_long = (v & (kLeafTruncated | kLeafHeavy)) || (v & kLeafCountMask) > kShortLeaves;
+        const bool is_long = (v & (kLeafTruncated | kLeafHeavy)) || (v & kLeafCountMask) > max_leaves;
         return is_long || (long long)*n_short < short_min;
     }
 };
@@ -1511,9 +1513,9 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
                                      wargs, 0, s));
             if (A.short_list) {  // short rays -> k_short, long ones -> k_warp (hit_list, count walk_counter[1])
                 XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.short_list, A.walk_counter, (int)n_slots,
-                                              IsShort{A.leaf_count}, s));
+                                              IsShort{A.leaf_count, A.short_leaves}, s));
                 XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.hit_list, A.walk_counter + 1, (int)n_slots,
-                                              IsLong{A.leaf_count, A.walk_counter, A.short_min}, s));
+                                              IsLong{A.leaf_count, A.walk_counter, A.short_min, A.short_leaves}, s));
                 using ShortFn = void (*)(RenderArgs, int64_t);
                 ShortFn sf;
                 if (g == 0) sf = iso ? (ShortFn)k_short<0, true, false> : (ShortFn)k_short<0, false, false>;

@@ -38,6 +38,8 @@ struct RenderArgs {
     int32_t* hit_list;                 // candidate rays (k_walk's work), then the long rays (k_warp's)
     int32_t* short_list;               // rays with a complete list of <= 8 leaves (k_short's work), or NULL
     long long short_min;               // k_short runs only for at least this many short rays (else k_warp takes them)
+    int short_leaves;                  // short ray: complete list of <= short_leaves leaves ...
+    float short_samples;               // ... and <= short_samples estimated samples
     float walk_tau_stop;               // k_walk stops listing once the opacity minorant passes this depth
     int use_lbvh;                      // XB_TRAVERSAL=lbvh: per-visit LBVH closest-hit queries (tile kernel)
     LbvhView vlb, ilb;                 // LBVHs of the volume / iso active sets

@@ -31,8 +31,11 @@ stream = torch.cuda.current_stream()
 def setv(v):
     """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N) | gD (guided grab divisor D)"""
     for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU",
-              "XB_TRAVERSAL", "XB_CAP_DIV", "XB_WALK_BUDGET", "XB_SHORT"):
+              "XB_TRAVERSAL", "XB_CAP_DIV", "XB_WALK_BUDGET", "XB_SHORT", "XB_SHORT_LEAVES", "XB_SHORT_SAMPLES"):
         os.environ.pop(k, None)
+    if v.startswith("sl") and "_" in v:  # slL_S: short-ray thresholds
+        os.environ["XB_SHORT_LEAVES"], os.environ["XB_SHORT_SAMPLES"] = v[2:].split("_")
+        return
     if v == "short":
         os.environ["XB_SHORT"] = "1"
     elif v == "noshort":
