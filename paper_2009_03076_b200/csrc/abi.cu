@@ -573,8 +573,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->outcnt = oc.dev;
         // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter, walk counter, hits]
         unsigned long long* scratch = nullptr;
-        XB_CUDA(cudaMallocAsync((void**)&scratch, 6 * sizeof(unsigned long long), s));
-        XB_CUDA(cudaMemsetAsync(scratch, 0, 6 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMallocAsync((void**)&scratch, 8 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMemsetAsync(scratch, 0, 8 * sizeof(unsigned long long), s));
         A->walk_counter = scratch + 4;
         unsigned long long* dstats = (stats || count_bytes) ? scratch : nullptr;
         A->stats = dstats;
@@ -593,6 +593,9 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->leaf_count = nullptr;
         A->short_list = nullptr;
         A->short_min = 0;
+        A->walk_cap1 = 0;
+        A->walk2_min = 0;
+        A->cut_list = nullptr;
         A->short_leaves = 8;
         A->short_samples = 24.f;
         A->leaf_cap = 0;
@@ -614,7 +617,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                 // C3's few very long walks set k_walk's length; C2's many long walks are cheaper in
                 // k_walk than in the frontier.  Neither the candidate count (similar in all three) nor a
                 // clock budget (tools/ab.py: budgets cost C2 15-25 %) separates them, so: a fixed 64.
-                const int cap = ec ? std::max(1, atoi(ec)) : 64;
+                const char* ec2 = getenv("XB_WALK_CAP2");
+                const int cap = ec ? std::max(1, atoi(ec)) : (ec2 ? std::max(1, atoi(ec2)) : 96);
                 const char* ed = getenv("XB_CAP_DIV");
                 A->cap_div = ed ? atoi(ed) : 0;
                 A->cap_min = 16;
@@ -623,9 +627,17 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                 const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
                 const size_t ns1 = std::max<size_t>(n_slots, 1);
                 const size_t res_words = 1 + 3 * 48;  // render.cu kResume
-                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 3 + res_words) * sizeof(int32_t), s));
+                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 4 + res_words) * sizeof(int32_t), s));
                 A->leaf_count = leaf_buf;
                 A->hit_list = leaf_buf + ns1;
+                // two-pass walk: pass 1 caps at 16 leaves; pass 2 continues the cap-cut walks to the
+                // list capacity (96) when there are >= 500 x SMs of them.  tools/ab.py, ms (C3 / C2 /
+                // C5): single cap 64: 1.39 / 6.72 / 3.45; 24+96: 1.22 / 6.54 / 3.75; 16+96: 1.20 /
+                // 6.55 / 3.64; 16+64: 1.19 / 6.73 / 3.51.
+                const char* e1 = getenv("XB_WALK_CAP1");
+                A->walk_cap1 = ec ? cap : (e1 ? std::max(1, atoi(e1)) : 16);
+                const char* e2 = getenv("XB_WALK2_MIN");
+                A->cut_list = leaf_buf + (3 + res_words + cap) * ns1;
                 // k_short for rays with <= 8 leaves and <= 24 estimated samples, used only when the
                 // frame has >= 1000 x SMs of them (decided on the device).  tools/ab.py, ms, forced on
                 // vs off: C3 (270K short rays) 1.56 vs 1.61, C5 (44K) 3.70 vs 3.40, C2 (57K) 6.82 vs
@@ -637,6 +649,7 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                 A->short_list = (esh && esh[0] == '0') ? nullptr : leaf_buf + 2 * ns1;
                 A->short_min = (esh && esh[0] == '1') ? 0 : 1000ll * sms;
                 A->short_leaves = getenv("XB_SHORT_LEAVES") ? atoi(getenv("XB_SHORT_LEAVES")) : 8;
+                A->walk2_min = e2 ? atoll(e2) : 500ll * sms;
                 A->short_samples = getenv("XB_SHORT_SAMPLES") ? (float)atof(getenv("XB_SHORT_SAMPLES")) : 24.f;
                 A->resume = leaf_buf + 3 * ns1;
                 A->leaves = leaf_buf + (3 + res_words) * ns1;

@@ -451,9 +451,10 @@ __device__ __forceinline__ void lattice(double ci, double co, double dt, double 
 
 constexpr int kWalkThreads = 128;
 constexpr int kWalkStack = 100;  // >= 3 x (Kd4 depth <= kKdStack / 2 + 1)
-constexpr int kLeafCountMask = 0x1fffffff;
+constexpr int kLeafCountMask = 0x0fffffff;
 constexpr int kLeafTruncated = 0x40000000;
 constexpr int kLeafHeavy = 0x20000000;  // > kShortSamples estimated samples (not for k_short)
+constexpr int kLeafTauStop = 0x10000000; // truncated by the opacity minorant (probably terminated)
 constexpr float kShortSamples = 24.f;  // defaults of RenderArgs.short_samples / short_leaves
 constexpr int kShortLeaves = 8;
 constexpr int kResume = 48;  // resume entries saved per truncated walk
@@ -527,149 +528,198 @@ __global__ void __launch_bounds__(kWalkThreads) k_classify(const __grid_constant
 // walk the candidate rays (hit_list[0, n)), one thread each; a walk lists at
 // most leaf_cap leaves (long walks are latency chains: k_warp continues those
 // rays with its parallel frontier)
+// The walk itself (front to back over the Kd4 tree from `code` with the
+// ordered stack st_*[0, sp_n)), listing leaves into out[count..cap); on a stop
+// it sets `flags` and saves the ordered remainder for k_warp.
+__device__ __forceinline__ void walk_leaves(const RenderArgs& A, int64_t slot, const Ray& r, const int sg[3],
+                                            double tmin, double tmax, int code, double tn, double tf, int* st_code,
+                                            float* st_tn, float* st_tf, int sp_n, int32_t* __restrict__ out,
+                                            int& count, int& flags, int cap, float& est) {
+    const SceneView& S = A.S;
+    const long long budget = A.walk_budget;
+    const float spc = (float)A.M.spc, tau_stop = A.walk_tau_stop;
+    float tau = 0.f;
+    const long long t_begin = clock64();
+    for (;;) {
+        if (code <= -2) {  // a leaf: list it
+            if (count == cap || (budget > 0 && clock64() - t_begin > budget)) {  // resume from this leaf
+                flags = kLeafTruncated;
+                save_resume(A, slot, code, tn, tf, st_code, st_tn, st_tf, sp_n);
+                break;
+            }
+            const int rid = -2 - code;
+            out[count++] = rid;
+            if (A.short_list && count <= A.short_leaves && est <= A.short_samples)  // samples ~ len/dt + 1
+                est += (float)((tf - tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
+            if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
+                tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;
+                if (tau > tau_stop) {
+                    flags = kLeafTruncated;
+                    save_resume(A, slot, kNoEntry, 0.0, 0.0, st_code, st_tn, st_tf, sp_n);
+                    break;
+                }
+            }
+        } else {
+            // expand the Kd4 node (same classification as kd_next / k_warp)
+            const Kd4Node nd = S.kd4[code];
+            const uint32_t msk = A.vmask4[code];
+            int oc[4];
+            double olo[4], ohi[4];
+            int no = 0;
+            int hs0 = 0, hs1 = 0, nh = 1;
+            double hn0 = tn, hf0 = tf, hn1 = 0.0, hf1 = 0.0;
+            {
+                const int ax = nd.axes & 3;
+                const double p = (double)nd.plane[0] * 0.5;
+                const double oa = sel3(ax, r.o);
+                const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
+                if (sa == 0) {
+                    hs0 = oa < p ? 0 : 1;
+                } else {
+                    const double tp = (p - oa) * sel3(ax, r.inv);
+                    const int ns_ = sa > 0 ? 0 : 1;
+                    if (tp >= tf) hs0 = ns_;
+                    else if (tp <= tn) hs0 = 1 - ns_;
+                    else { hs0 = ns_; hf0 = tp; hs1 = 1 - ns_; hn1 = tp; hf1 = tf; nh = 2; }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                if (h < nh) {
+                    const int sd = h ? hs1 : hs0;
+                    const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
+                    const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
+                    int s0 = 2 * sd, s1 = -1;
+                    double a0 = hn, b0 = hf, a1 = 0.0, b1 = 0.0;
+                    if (ax != 3) {
+                        const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
+                        const double oa = sel3(ax, r.o);
+                        const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
+                        if (sa == 0) {
+                            s0 = 2 * sd + (oa < p ? 0 : 1);
+                        } else {
+                            const double tp = (p - oa) * sel3(ax, r.inv);
+                            const int nq = sa > 0 ? 0 : 1;
+                            if (tp >= b0) s0 = 2 * sd + nq;
+                            else if (tp <= a0) s0 = 2 * sd + 1 - nq;
+                            else { s0 = 2 * sd + nq; b0 = tp; s1 = 2 * sd + 1 - nq; a1 = tp; b1 = hf; }
+                        }
+                    }
+                    if (((msk >> s0) & 1) && b0 > tmin && a0 < tmax) {
+                        oc[no] = kd4_child(nd, s0); olo[no] = a0; ohi[no] = b0; no++;
+                    }
+                    if (s1 >= 0 && ((msk >> s1) & 1) && b1 > tmin && a1 < tmax) {
+                        oc[no] = kd4_child(nd, s1); olo[no] = a1; ohi[no] = b1; no++;
+                    }
+                }
+            }
+            if (no > 0) {  // continue with the nearest child, stack the others farthest-first
+                if (sp_n + no - 1 > kWalkStack) __trap();  // depth-bounded: <= 3 per Kd4 level
+                for (int c = no - 1; c >= 1; c--) {
+                    st_code[sp_n] = oc[c];
+                    st_tn[sp_n] = __double2float_rd(olo[c]);
+                    st_tf[sp_n] = __double2float_ru(ohi[c]);
+                    sp_n++;
+                }
+                code = oc[0];
+                tn = olo[0];
+                tf = ohi[0];
+                continue;
+            }
+        }
+        if (sp_n == 0) break;
+        --sp_n;
+        code = st_code[sp_n];
+        tn = (double)st_tn[sp_n];
+        tf = (double)st_tf[sp_n];
+    }
+}
+
 __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const SceneView& S = A.S;
     const int64_t n_cand = (int64_t)A.walk_counter[1];
-    // Adaptive leaf cap: with few candidate rays (a small object on screen) the
-    // kernel's length is the longest walk, so walks are cut short early and
-    // k_warp's parallel frontier resumes them; with many, long lists pay off.
-    const int cap = A.cap_div > 0 ? (int)max((int64_t)A.cap_min, min((int64_t)A.leaf_cap, n_cand / A.cap_div))
-                                  : A.leaf_cap;
-    // ... and every walk has a latency budget (clock cycles): a walk whose node
-    // loads keep missing L2 is cut and resumed by k_warp's parallel frontier.
-    // Results do not depend on where a walk stops (resume is exact).
-    const long long budget = A.walk_budget;
+    // Pass 1 lists at most walk_cap1 leaves per ray: a few very long walks (latency
+    // chains of node loads) would otherwise set the kernel's length; k_walk2
+    // continues the cap-truncated walks when there are many of them.
+    const int cap = A.walk_cap1;
     for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < n_cand;
          ci += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t slot = A.hit_list[ci];
-    int count = 0, flags = 0;
-    {
+        const int64_t slot = A.hit_list[ci];
+        int count = 0, flags = 0;
         const SlotPix spx = slot_pixel(A, slot);
-        bool clip_ok = false;
         if (spx.live) {
             Ray r;
             pixel_ray(A, spx.x, spx.y, r);
             double tmin = 0.0, tmax = kTFar;
             clip_ray(A.M, r, tmin, tmax);
-            clip_ok = tmin < tmax;
+            const bool clip_ok = tmin < tmax;
             if (clip_ok && A.M.iso_on) tmax = A.iso_tend[slot];
             double a = 0.0, b = -1.0;
             slab_h(S.root_lo, S.root_hi, r, a, b);
             if (clip_ok && S.n_kd > 0 && a <= b && A.vflags[0]) {
-                int32_t* __restrict__ out = A.leaves + slot * (int64_t)A.leaf_cap;
                 int st_code[kWalkStack];
                 float st_tn[kWalkStack], st_tf[kWalkStack];
-                int sp_n = 0;
-                int code = S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2);
-                double tn = a, tf = b;
                 int sg[3];
                 for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
-                const float spc = (float)A.M.spc, tau_stop = A.walk_tau_stop;
-                float tau = 0.f, est = 0.f;
-                const long long t_begin = clock64();
-                for (;;) {
-                    if (code <= -2) {  // a leaf: list it
-                        if (count == cap || (budget > 0 && clock64() - t_begin > budget)) {  // resume from this leaf
-                            flags = kLeafTruncated;
-                            save_resume(A, slot, code, tn, tf, st_code, st_tn, st_tf, sp_n);
-                            break;
-                        }
-                        const int rid = -2 - code;
-                        out[count++] = rid;
-                        if (A.short_list && count <= A.short_leaves && est <= A.short_samples)  // samples ~ len/dt + 1
-                            est += (float)((tf - tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
-                        if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
-                            tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;
-                            if (tau > tau_stop) {
-                                flags = kLeafTruncated;
-                                save_resume(A, slot, kNoEntry, 0.0, 0.0, st_code, st_tn, st_tf, sp_n);
-                                break;
-                            }
-                        }
-                    } else {
-                        // expand the Kd4 node (same classification as kd_next / k_warp)
-                        const Kd4Node nd = S.kd4[code];
-                        const uint32_t msk = A.vmask4[code];
-                        int oc[4];
-                        double olo[4], ohi[4];
-                        int no = 0;
-                        int hs0 = 0, hs1 = 0, nh = 1;
-                        double hn0 = tn, hf0 = tf, hn1 = 0.0, hf1 = 0.0;
-                        {
-                            const int ax = nd.axes & 3;
-                            const double p = (double)nd.plane[0] * 0.5;
-                            const double oa = sel3(ax, r.o);
-                            const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
-                            if (sa == 0) {
-                                hs0 = oa < p ? 0 : 1;
-                            } else {
-                                const double tp = (p - oa) * sel3(ax, r.inv);
-                                const int ns_ = sa > 0 ? 0 : 1;
-                                if (tp >= tf) hs0 = ns_;
-                                else if (tp <= tn) hs0 = 1 - ns_;
-                                else { hs0 = ns_; hf0 = tp; hs1 = 1 - ns_; hn1 = tp; hf1 = tf; nh = 2; }
-                            }
-                        }
-#pragma unroll
-                        for (int h = 0; h < 2; h++) {
-                            if (h < nh) {
-                                const int sd = h ? hs1 : hs0;
-                                const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
-                                const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
-                                int s0 = 2 * sd, s1 = -1;
-                                double a0 = hn, b0 = hf, a1 = 0.0, b1 = 0.0;
-                                if (ax != 3) {
-                                    const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
-                                    const double oa = sel3(ax, r.o);
-                                    const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
-                                    if (sa == 0) {
-                                        s0 = 2 * sd + (oa < p ? 0 : 1);
-                                    } else {
-                                        const double tp = (p - oa) * sel3(ax, r.inv);
-                                        const int nq = sa > 0 ? 0 : 1;
-                                        if (tp >= b0) s0 = 2 * sd + nq;
-                                        else if (tp <= a0) s0 = 2 * sd + 1 - nq;
-                                        else { s0 = 2 * sd + nq; b0 = tp; s1 = 2 * sd + 1 - nq; a1 = tp; b1 = hf; }
-                                    }
-                                }
-                                if (((msk >> s0) & 1) && b0 > tmin && a0 < tmax) {
-                                    oc[no] = kd4_child(nd, s0); olo[no] = a0; ohi[no] = b0; no++;
-                                }
-                                if (s1 >= 0 && ((msk >> s1) & 1) && b1 > tmin && a1 < tmax) {
-                                    oc[no] = kd4_child(nd, s1); olo[no] = a1; ohi[no] = b1; no++;
-                                }
-                            }
-                        }
-                        if (no > 0) {  // continue with the nearest child, stack the others farthest-first
-                            if (sp_n + no - 1 > kWalkStack) __trap();  // depth-bounded: <= 3 per Kd4 level
-                            for (int c = no - 1; c >= 1; c--) {
-                                st_code[sp_n] = oc[c];
-                                st_tn[sp_n] = __double2float_rd(olo[c]);
-                                st_tf[sp_n] = __double2float_ru(ohi[c]);
-                                sp_n++;
-                            }
-                            code = oc[0];
-                            tn = olo[0];
-                            tf = ohi[0];
-                            continue;
-                        }
-                    }
-                    if (sp_n == 0) break;
-                    --sp_n;
-                    code = st_code[sp_n];
-                    tn = (double)st_tn[sp_n];
-                    tf = (double)st_tf[sp_n];
-                }
+                float est = 0.f;
+                walk_leaves(A, slot, r, sg, tmin, tmax, S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2), a, b, st_code, st_tn,
+                            st_tf, 0, A.leaves + slot * (int64_t)A.leaf_cap, count, flags, cap, est);
                 if (est > A.short_samples) flags |= kLeafHeavy;
             }
+            A.leaf_count[slot] = count | flags;
+            if (count == 0 && !flags) write_empty_pixel(A, slot, spx.out, true);  // no active region on the ray
+        } else {
+            A.leaf_count[slot] = 0;
         }
-        A.leaf_count[slot] = count | flags;
-        if (count == 0 && !flags) write_empty_pixel(A, slot, spx.out, true);  // no active region on the ray
-    }
     }
     (void)n_slots;
 }
 
+// Pass 2: continue the walks pass 1 cut at walk_cap1 (not those stopped by the
+// opacity minorant) up to leaf_cap, from their saved ordered remainder — only
+// when there are at least walk2_min of them (decided on the device): many long
+// rays (C2, C5) are cheaper here than in k_warp's frontier; a few (C3) are not.
+struct IsCapCut {
+    const int32_t* c;
+    __device__ __forceinline__ bool operator()(const int32_t i) const {
+        const int v = c[i];
+        return (v & kLeafTruncated) && !(v & kLeafTauStop);
+    }
+};
+
+__global__ void __launch_bounds__(kWalkThreads) k_walk2(const __grid_constant__ RenderArgs A, int64_t n_slots) {
+    const int64_t n_cut = (int64_t)A.walk_counter[2];
+    if (n_cut < A.walk2_min) return;
+    const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (ci >= n_cut) return;
+    const int64_t slot = A.cut_list[ci];
+    int32_t* res = A.resume + slot * (int64_t)(1 + 3 * kResume);
+    const int m = res[0];
+    if (m <= 0) return;  // remainder not saved: k_warp restarts at the root
+    const SlotPix spx = slot_pixel(A, slot);
+    Ray r;
+    pixel_ray(A, spx.x, spx.y, r);
+    double tmin = 0.0, tmax = kTFar;
+    clip_ray(A.M, r, tmin, tmax);
+    if (A.M.iso_on) tmax = A.iso_tend[slot];
+    int st_code[kWalkStack];
+    float st_tn[kWalkStack], st_tf[kWalkStack];
+    int sp_n = 0;
+    for (int k = m - 1; k >= 1; k--, sp_n++) {  // entries 1.. on the stack, entry 1 on top
+        st_code[sp_n] = res[1 + 3 * k];
+        st_tn[sp_n] = __int_as_float(res[2 + 3 * k]);
+        st_tf[sp_n] = __int_as_float(res[3 + 3 * k]);
+    }
+    int sg[3];
+    for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
+    const int lraw = A.leaf_count[slot];
+    int count = lraw & kLeafCountMask, flags = lraw & kLeafHeavy;
+    float est = INFINITY;
+    walk_leaves(A, slot, r, sg, tmin, tmax, res[1], (double)__int_as_float(res[2]), (double)__int_as_float(res[3]),
+                st_code, st_tn, st_tf, sp_n, A.leaves + slot * (int64_t)A.leaf_cap, count, flags, A.leaf_cap, est);
+    A.leaf_count[slot] = count | flags;
+    (void)n_slots;
+}
 // hit rays (leaf_count != 0) -> k_walk's work list, in slot (screen-tile) order
 struct HasLeaves {
     const int32_t* c;
@@ -1511,6 +1561,12 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             // one thread per candidate (blocks past the device-side count exit at once)
             XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
                                      wargs, 0, s));
+            if (A.cut_list && A.walk_cap1 < A.leaf_cap) {  // pass 2 over the cap-cut walks
+                XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.cut_list, A.walk_counter + 2, (int)n_slots,
+                                              IsCapCut{A.leaf_count}, s));
+                XB_CUDA(cudaLaunchKernel((const void*)k_walk2, dim3(grid_for(n_slots, kWalkThreads)),
+                                         dim3(kWalkThreads), wargs, 0, s));
+            }
             if (A.short_list) {  // short rays -> k_short, long ones -> k_warp (hit_list, count walk_counter[1])
                 XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.short_list, A.walk_counter, (int)n_slots,
                                               IsShort{A.leaf_count, A.short_leaves}, s));

@@ -29,7 +29,10 @@ struct RenderArgs {
     int grab_div, grab_fixed;          // k_warp grab schedule (launch_render)
     int32_t* leaves;                   // k_walk -> k_warp: per slot leaf_cap region ids in ray order (or NULL)
     int32_t* leaf_count;               // per slot: count | 0x40000000 when truncated
-    int leaf_cap;                      // list capacity per slot
+    int leaf_cap;                      // list capacity per slot (k_walk2's cap)
+    int walk_cap1;                     // k_walk's cap (pass 1)
+    long long walk2_min;               // k_walk2 runs only for at least this many cap-cut walks
+    int32_t* cut_list;                 // walks cut at walk_cap1 (k_walk2's work)
     int cap_div, cap_min;              // k_walk's effective cap = clamp(n_candidates / cap_div, cap_min, leaf_cap)
     long long walk_budget;             // k_walk: clock cycles per walk before it hands over (0 = none)
     int32_t* resume;                   // per slot: k_walk's ordered remainder when truncated (1 + 3 x kResume words)
