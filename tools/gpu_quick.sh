@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for c in c3 c2 c5; do timeout 300 python tools/ab.py $c warp,w2_16_64,w2_16_96,w2_16_128,w2_24_64 6 > gpurun_out/ab_w3_$c.log 2>&1; grep median gpurun_out/ab_w3_$c.log; done
+timeout 1200 python -m pytest tests/test_gpu_parity.py -q -m gpu -x --timeout 900 -k "acceptance or frames_match or tiled" > gpurun_out/pt_w4.log 2>&1; tail -3 gpurun_out/pt_w4.log
