@@ -539,10 +539,15 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             }
         }
         A->vqmin = vol->a.qmin.n ? vol->a.qmin.p : nullptr;
+        A->wflags = A->vflags;
+        A->wmask4 = A->vmask4;
+        A->wqmin = A->vqmin;
+        A->walk_iso = 0;
         fill_march(A->M, mp);
         A->M.iso_on = (mp->iso_on && iso) ? 1 : 0;
         if (A->M.iso_on) check_active(iso, r, "iso");
         A->iflags = A->M.iso_on ? iso->a.flags.p : vol->a.flags.p;
+        A->imask4 = A->M.iso_on ? iso->a.mask4.p : vol->a.mask4.p;
         A->W = cam->width;
         A->H = cam->height;
         for (int a = 0; a < 3; a++) {

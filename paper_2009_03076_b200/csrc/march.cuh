@@ -1096,13 +1096,23 @@ __device__ __forceinline__ void count_eval(RayStats& st, int nids, const Accum& 
     if (COUNT) st.bytes += 16 * (int64_t)nids + 4 * A.n_nz;
 }
 
+// a ray's active regions listed in ray order by k_walk; `trunc`: the list stops
+// early and the k-d walk continues from the query point
+struct IsoList {
+    const int32_t* list;
+    int n;
+    bool trunc;
+};
+
 // _iso_ray, R/render.py:456-518
 template <bool COUNT>
 __device__ bool iso_ray(const SceneView& S, const uint8_t* __restrict__ iflags, const MarchConst& M, const Ray& r,
                         double tmin, double tmax, double rho, double& t_hit, double g[3], RayStats& st,
-                        const LbvhView* lb = nullptr) {
+                        const LbvhView* lb = nullptr, const IsoList* lst = nullptr) {
     KdWalk w;
-    kd_begin(S, r, w);
+    int lpos = 0;
+    bool walking = lst == nullptr;
+    if (walking) kd_begin(S, r, w);
     double t = tmin;
     const double iso = M.iso_value;
     g[0] = g[1] = g[2] = 0.0;
@@ -1110,10 +1120,33 @@ __device__ bool iso_ray(const SceneView& S, const uint8_t* __restrict__ iflags, 
     for (;;) {
         int rid;
         double t_in, t_out;
-        // next region: ordered k-d walk, or a fresh LBVH closest-hit query (the reference's way)
-        if (!(lb ? lbvh_next_hit(S, *lb, r, t, tmax, rid, t_in, t_out)
-                 : kd_next(S, iflags, r, w, t, tmax, rid, t_in, t_out)))
-            return false;
+        // next region: k_walk's list (exact slab + restart chain), the ordered k-d
+        // walk, or a fresh LBVH closest-hit query (the reference's way)
+        bool got = false;
+        if (!walking) {
+            while (lpos < lst->n) {
+                const int reg = lst->list[lpos++];
+                const RegionRec q = S.rec[reg];
+                double r_in, r_out;
+                slab_h(q.lo, q.hi, r, r_in, r_out);
+                const double ci = r_in > t ? r_in : t, co = r_out < tmax ? r_out : tmax;
+                if (ci < co) {
+                    rid = reg;
+                    t_in = ci;
+                    t_out = co;
+                    got = true;
+                    break;
+                }
+            }
+            if (!got && lst->trunc) {  // continue with the k-d walk (a walk from the root culls by t: exact)
+                walking = true;
+                kd_begin(S, r, w);
+            }
+        }
+        if (walking)
+            got = lb ? lbvh_next_hit(S, *lb, r, t, tmax, rid, t_in, t_out)
+                     : kd_next(S, iflags, r, w, t, tmax, rid, t_in, t_out);
+        if (!got) return false;
         const RegionRec rr = S.rec[rid];
         const int nids = rr.meta & 0xffffff;
         const int32_t* ids = S.rids + rr.ids_begin;

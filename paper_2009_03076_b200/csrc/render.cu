@@ -15,6 +15,7 @@
 //
 // The per-pixel arithmetic is `_render_kernel` (R/render.py:521-578) in both.
 #include <cmath>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
@@ -519,8 +520,16 @@ __global__ void __launch_bounds__(kWalkThreads) k_classify(const __grid_constant
         const bool clip_ok = tmin < tmax;
         double a = 0.0, b = -1.0;
         slab_h(S.root_lo, S.root_hi, r, a, b);
-        cand = clip_ok && S.n_kd > 0 && a <= b && A.vflags[0];
-        if (!cand) write_empty_pixel(A, slot, spx.out, clip_ok);
+        cand = clip_ok && S.n_kd > 0 && a <= b && A.wflags[0];
+        if (A.walk_iso) {  // iso phase: default "no hit" (t_end = clip end, no shade)
+            A.iso_tend[slot] = tmax;
+            A.iso_shade[slot] = -1.0;
+        } else if (!cand) {
+            write_empty_pixel(A, slot, spx.out, clip_ok);
+        }
+    } else if (A.walk_iso) {
+        A.iso_tend[slot] = -1.0;
+        A.iso_shade[slot] = -1.0;
     }
     A.leaf_count[slot] = cand ? -1 : 0;
 }
@@ -551,8 +560,8 @@ __device__ __forceinline__ void walk_leaves(const RenderArgs& A, int64_t slot, c
             out[count++] = rid;
             if (A.short_list && count <= A.short_leaves && est <= A.short_samples)  // samples ~ len/dt + 1
                 est += (float)((tf - tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
-            if (A.vqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
-                tau += __ldg(A.vqmin + rid) * (float)(tf - tn) * spc;
+            if (A.wqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
+                tau += __ldg(A.wqmin + rid) * (float)(tf - tn) * spc;
                 if (tau > tau_stop) {
                     flags = kLeafTruncated;
                     save_resume(A, slot, kNoEntry, 0.0, 0.0, st_code, st_tn, st_tf, sp_n);
@@ -562,7 +571,7 @@ __device__ __forceinline__ void walk_leaves(const RenderArgs& A, int64_t slot, c
         } else {
             // expand the Kd4 node (same classification as kd_next / k_warp)
             const Kd4Node nd = S.kd4[code];
-            const uint32_t msk = A.vmask4[code];
+            const uint32_t msk = A.wmask4[code];
             int oc[4];
             double olo[4], ohi[4];
             int no = 0;
@@ -653,10 +662,10 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
             double tmin = 0.0, tmax = kTFar;
             clip_ray(A.M, r, tmin, tmax);
             const bool clip_ok = tmin < tmax;
-            if (clip_ok && A.M.iso_on) tmax = A.iso_tend[slot];
+            if (clip_ok && A.M.iso_on && !A.walk_iso) tmax = A.iso_tend[slot];
             double a = 0.0, b = -1.0;
             slab_h(S.root_lo, S.root_hi, r, a, b);
-            if (clip_ok && S.n_kd > 0 && a <= b && A.vflags[0]) {
+            if (clip_ok && S.n_kd > 0 && a <= b && A.wflags[0]) {
                 int st_code[kWalkStack];
                 float st_tn[kWalkStack], st_tf[kWalkStack];
                 int sg[3];
@@ -667,7 +676,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
                 if (est > A.short_samples) flags |= kLeafHeavy;
             }
             A.leaf_count[slot] = count | flags;
-            if (count == 0 && !flags) write_empty_pixel(A, slot, spx.out, true);  // no active region on the ray
+            if (count == 0 && !flags && !A.walk_iso) write_empty_pixel(A, slot, spx.out, true);  // no active region
         } else {
             A.leaf_count[slot] = 0;
         }
@@ -701,7 +710,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk2(const __grid_constant__ 
     pixel_ray(A, spx.x, spx.y, r);
     double tmin = 0.0, tmax = kTFar;
     clip_ray(A.M, r, tmin, tmax);
-    if (A.M.iso_on) tmax = A.iso_tend[slot];
+    if (A.M.iso_on && !A.walk_iso) tmax = A.iso_tend[slot];
     int st_code[kWalkStack];
     float st_tn[kWalkStack], st_tf[kWalkStack];
     int sp_n = 0;
@@ -720,6 +729,172 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk2(const __grid_constant__ 
     A.leaf_count[slot] = count | flags;
     (void)n_slots;
 }
+// Iso phase: one thread per iso-candidate ray runs _iso_ray (R/render.py:456-518)
+// over the regions k_walk listed for the iso active set, continuing with the
+// k-d walk from the root when the list was truncated (exact either way).
+template <bool COUNT>
+__global__ void __launch_bounds__(kWalkThreads) k_iso_march(const __grid_constant__ RenderArgs A, int64_t n_slots) {
+    const int64_t n_cand = (int64_t)A.walk_counter[1];
+    const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (ci >= n_cand) return;
+    const int64_t slot = A.hit_list[ci];
+    const SlotPix sp = slot_pixel(A, slot);
+    Ray r;
+    pixel_ray(A, sp.x, sp.y, r);
+    const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
+    double tmin = 0.0, tmax = kTFar;
+    clip_ray(A.M, r, tmin, tmax);
+    const int lraw = A.leaf_count[slot];
+    const IsoList lst{A.leaves + slot * (int64_t)A.leaf_cap, lraw & kLeafCountMask, (lraw & kLeafTruncated) != 0};
+    RayStats st = {0, 0, 0};
+    double g[3], th = 0.0;
+    if (iso_ray<COUNT>(A.S, A.iflags, A.M, r, tmin, tmax, rho, th, g, st, nullptr, &lst)) {
+        A.iso_tend[slot] = th;
+        A.iso_shade[slot] = shade_factor(g, r);
+    }
+    if (COUNT && st.bytes) atomicAdd(&A.stats[2], (unsigned long long)st.bytes);
+    (void)n_slots;
+}
+
+// Iso phase, warp per ray: _iso_ray (R/render.py:456-518) evaluates f = value
+// - iso at t_in and at every lattice point of each iso-active region until the
+// sign changes; a region's lattice can hold thousands of points (its step is
+// half its finest cell width), so the warp evaluates 32 consecutive points at
+// once and takes the first sign change (ballot) — the same point the
+// sequential loop finds — then bisects 16 times and takes the analytic normal.
+template <bool COUNT>
+__global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant__ RenderArgs A, int64_t n_slots) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const SceneView& S = A.S;
+    const int64_t n_cand = (int64_t)A.walk_counter[1];
+    const double iso = A.M.iso_value;
+    unsigned long long bytes = 0;
+    for (;;) {
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(A.work_counter, 1ull);
+        c = __shfl_sync(FULL, c, 0);
+        if ((int64_t)c >= n_cand) break;
+        const int64_t slot = A.hit_list[c];
+        const SlotPix sp = slot_pixel(A, slot);
+        Ray r;
+        pixel_ray(A, sp.x, sp.y, r);
+        const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
+        double tmin = 0.0, tmax = kTFar;
+        clip_ray(A.M, r, tmin, tmax);
+        const int lraw = A.leaf_count[slot];
+        const int32_t* __restrict__ list = A.leaves + slot * (int64_t)A.leaf_cap;
+        const int lcount = lraw & kLeafCountMask;
+        const bool ltrunc = (lraw & kLeafTruncated) != 0;
+        int lpos = 0;
+        bool walking = false;
+        KdWalk w;
+        double t = tmin;
+        for (;;) {
+            // next region (all lanes compute the same): the list, then the k-d walk
+            int rid = -1;
+            double ci = 0.0, co = 0.0;
+            bool got = false;
+            if (!walking) {
+                while (lpos < lcount) {
+                    const int reg = list[lpos++];
+                    const RegionRec q = S.rec[reg];
+                    double r_in, r_out;
+                    slab_h(q.lo, q.hi, r, r_in, r_out);
+                    const double a = r_in > t ? r_in : t, b = r_out < tmax ? r_out : tmax;
+                    if (a < b) {
+                        rid = reg; ci = a; co = b; got = true;
+                        break;
+                    }
+                }
+                if (!got && ltrunc) {
+                    walking = true;
+                    kd_begin(S, r, w);
+                }
+            }
+            if (walking) got = kd_next(S, A.iflags, r, w, t, tmax, rid, ci, co);
+            if (!got) break;
+            const RegionRec rr = S.rec[rid];
+            const int nids = rr.meta & 0xffffff;
+            const int32_t* ids = S.rids + rr.ids_begin;
+            if (COUNT && lane == 0) bytes += 32 + 4 * (unsigned long long)nids;
+            const double dt = A.M.lv_dt[rr.meta >> 24];
+            double kf;
+            int cnt;
+            lattice(ci, co, dt, rho, kf, cnt);  // points p_0 = t_in, p_1..p_cnt (p_cnt = t_out)
+            double carry_f = 0.0, carry_t = ci;
+            bool carry_ok = false, hit = false;
+            double th = 0.0, g[3] = {0.0, 0.0, 0.0};
+            for (int base = 0; base <= cnt && !hit; base += 32) {
+                const int i = base + lane;
+                const bool act = i <= cnt;
+                const double ti = i == 0 ? ci : (i >= cnt ? co : dt * ((kf + (double)(i - 1)) + rho));
+                bool ok = false;
+                double f = 0.0;
+                if (act) {
+                    Accum Q;
+                    gather<false>(S, ids, nids, r.o[0] + ti * r.d[0], r.o[1] + ti * r.d[1], r.o[2] + ti * r.d[2], Q);
+                    ok = Q.den > kEpsWeight;
+                    f = ok ? Q.num / Q.den - iso : 0.0;
+                    if (COUNT) bytes += 16 * (unsigned long long)nids + 4 * (unsigned long long)Q.n_nz;
+                }
+                double pf = __shfl_up_sync(FULL, f, 1), pt = __shfl_up_sync(FULL, ti, 1);
+                bool pok = __shfl_up_sync(FULL, (int)ok, 1) != 0;
+                if (lane == 0) { pf = carry_f; pt = carry_t; pok = carry_ok; }
+                const bool change = act && i >= 1 && pok && ok && ((pf <= 0.0 && f >= 0.0) || (pf >= 0.0 && f <= 0.0)) &&
+                                    !(pf == 0.0 && f == 0.0);
+                const unsigned m = __ballot_sync(FULL, change);
+                if (m) {
+                    const int j = __ffs(m) - 1;
+                    if (COUNT) {  // evaluations after the first change were not made by the reference
+                        const int lastv = min(31, cnt - base);
+                        if (lane > j && lane <= lastv) bytes -= 16 * (unsigned long long)nids;  // n_nz part below
+                    }
+                    double lo_t = __shfl_sync(FULL, pt, j), hi_t = __shfl_sync(FULL, ti, j);
+                    double flo = __shfl_sync(FULL, pf, j);
+                    for (int it = 0; it < 16; it++) {  // the reference's bisection, every lane in step
+                        const double mid = 0.5 * (lo_t + hi_t);
+                        Accum Q;
+                        gather<false>(S, ids, nids, r.o[0] + mid * r.d[0], r.o[1] + mid * r.d[1], r.o[2] + mid * r.d[2],
+                                      Q);
+                        if (COUNT && lane == 0) bytes += 16 * (unsigned long long)nids + 4 * (unsigned long long)Q.n_nz;
+                        const double fm = Q.den > kEpsWeight ? Q.num / Q.den - iso : 0.0;
+                        if ((flo <= 0.0 && fm <= 0.0) || (flo >= 0.0 && fm >= 0.0)) { lo_t = mid; flo = fm; }
+                        else hi_t = mid;
+                    }
+                    th = 0.5 * (lo_t + hi_t);
+                    Accum Q;
+                    gather<true>(S, ids, nids, r.o[0] + th * r.d[0], r.o[1] + th * r.d[1], r.o[2] + th * r.d[2], Q);
+                    if (Q.den > kEpsWeight) {
+                        const double d2 = Q.den * Q.den;
+                        for (int a = 0; a < 3; a++) g[a] = (Q.dn[a] * Q.den - Q.gnum * Q.dd[a]) / d2;
+                    }
+                    hit = true;
+                    break;
+                }
+                const int lastv = min(31, cnt - base);
+                carry_f = __shfl_sync(FULL, f, lastv);
+                carry_t = __shfl_sync(FULL, ti, lastv);
+                carry_ok = __shfl_sync(FULL, (int)ok, lastv) != 0;
+            }
+            if (hit) {
+                if (lane == 0) {
+                    A.iso_tend[slot] = th;
+                    A.iso_shade[slot] = shade_factor(g, r);
+                }
+                break;
+            }
+            t = restart_t(co);
+            if (t >= tmax) break;
+        }
+    }
+    if (COUNT) {
+        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(FULL, bytes, o);
+        if (lane == 0 && bytes) atomicAdd(&A.stats[2], bytes);
+    }
+    (void)n_slots;
+}
+
 // hit rays (leaf_count != 0) -> k_walk's work list, in slot (screen-tile) order
 struct HasLeaves {
     const int32_t* c;
@@ -1503,15 +1678,57 @@ static int kernel_choice() {
     return 0;
 }
 
+// slots i in [0, n) with pred(i), in order -> out, count -> *n_out (device)
+template <class Pred>
+static void select_flagged(int32_t* out, unsigned long long* n_out, Pred pred, int64_t n, cudaStream_t s) {
+    size_t tb = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    XB_CUDA(cub::DeviceSelect::If(nullptr, tb, it, out, n_out, (int)n, pred, s));
+    void* tmp = nullptr;
+    XB_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 16), s));
+    XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, out, n_out, (int)n, pred, s));
+    XB_CUDA(cudaFreeAsync(tmp, s));
+}
+
 void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaStream_t s) {
     if (n_tiles_local <= 0) return;
     const bool iso = A.M.iso_on != 0;
     const int g = grad_index(A.M.grad_mode);
     const int64_t n_slots = n_tiles_local * kTileW * kTileH;
-    if (iso) {
+    if (iso && (!A.leaves || kernel_choice() != 0)) {  // per-lane iso pass (frame / tile / LBVH paths)
         void* args[] = {(void*)&A, (void*)&n_slots};
         const void* fn = count ? (const void*)k_iso_pass<true> : (const void*)k_iso_pass<false>;
         XB_CUDA(cudaLaunchKernel(fn, dim3(grid_for(n_slots, 128)), dim3(128), args, 0, s));
+    } else if (iso) {
+        // iso phase through the walk machinery: classify, select, walk the iso set, march
+        RenderArgs* Ai = new RenderArgs(A);
+        std::unique_ptr<RenderArgs> hold(Ai);
+        Ai->walk_iso = 1;
+        Ai->wflags = A.iflags;
+        Ai->wmask4 = A.imask4;
+        Ai->wqmin = nullptr;
+        Ai->short_list = nullptr;
+        Ai->walk_cap1 = std::min(A.leaf_cap, 16);
+        void* iargs[] = {(void*)Ai, (void*)&n_slots};
+        XB_CUDA(cudaLaunchKernel((const void*)k_classify, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
+                                 iargs, 0, s));
+        select_flagged(A.hit_list, A.walk_counter + 1, HasLeaves{A.leaf_count}, n_slots, s);
+        XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads), iargs,
+                                 0, s));
+        if (getenv("XB_ISO_LANE")) {  // A/B: one thread per iso ray
+            const void* mf = count ? (const void*)k_iso_march<true> : (const void*)k_iso_march<false>;
+            XB_CUDA(cudaLaunchKernel(mf, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads), iargs, 0, s));
+        } else {
+            const void* mf = count ? (const void*)k_iso_warp<true> : (const void*)k_iso_warp<false>;
+            int dev = 0, sms = 0, per_sm = 0;
+            XB_CUDA(cudaGetDevice(&dev));
+            XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mf, kWarpThreads, 0));
+            XB_CUDA(cudaLaunchKernel(mf, dim3((unsigned)std::max(1, sms * std::max(per_sm, 1))), dim3(kWarpThreads),
+                                     iargs, 0, s));
+            // k_warp's ray counter is shared: reset it for the volume phase
+            XB_CUDA(cudaMemsetAsync(A.work_counter, 0, sizeof(unsigned long long), s));
+        }
     }
     const int kc = A.M.use_tree ? 2 : kernel_choice();  // cell location: the one-thread-per-pixel kernel
     {  // k_warp guided ray-grab schedule (tuning knob XB_GRAB_DIV)

@@ -15,6 +15,12 @@ struct RenderArgs {
     SceneView S;
     const uint8_t* vflags;  // per k-d node: subtree holds an active volume region
     const uint8_t* vmask4;  // per Kd4 node: active bit per child slot (k_warp)
+    const uint8_t* imask4;  // same for the iso set
+    // the active set k_classify / k_walk walk: the volume set, or the iso set in the iso phase
+    const uint8_t* wflags;
+    const uint8_t* wmask4;
+    const float* wqmin;
+    int walk_iso;
     const uint8_t* iflags;  // same for the iso predicate
     MarchConst M;
     int W, H;

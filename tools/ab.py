@@ -19,7 +19,7 @@ cells = bench.make_cells(cfg)
 model, _ = build_bricks(cells)
 regions = build_regions(model)
 tf = bench.tf_for(model.value_range(0), cfg)
-scene = build_scene(model, regions, tf)
+scene = build_scene(model, regions, tf, iso_value=cfg.get("iso"))
 cam = bench.camera_for(regions.bounds, cfg, 0)
 params = MarchParams(seed=0, gradient_mode=cfg["gradient"])
 W, H = cfg["res"]
