@@ -418,14 +418,19 @@ def run_config(args, cfg, cfg_name, with_extras):
 
     # ---- e2e through the public API: host output, stats read back every frame
     e2e = None
+    e2e_all = None
     if with_extras and not args.profile:
         if world == 1:
-            for _ in range(3):  # warm-up: page-locked output blocks enter the host allocator's cache
-                render_frame(scene, cam, tf, params)
+            fr = None
+            for _ in range(3):  # warm-up as the timed loop: the previous frame stays alive while the next
+                fr = render_frame(scene, cam, tf, params)  # renders (two page-locked blocks in the cache)
             torch.cuda.synchronize()
+            e2e_all = []
             te = time.perf_counter()
             for _ in range(args.steps):
+                tq = time.perf_counter()
                 fr = render_frame(scene, cam, tf, params)
+                e2e_all.append((time.perf_counter() - tq) * 1e3)
             te = time.perf_counter() - te
             assert fr.stats.samples == tot_samples
             e2e_ms = te / args.steps * 1000.0
@@ -451,6 +456,7 @@ def run_config(args, cfg, cfg_name, with_extras):
         e2e = {"value": 1000.0 / e2e_ms, "unit": "frames/s",
                "h2d_bytes_per_step": ctypes.sizeof(NN.XbMarch) + ctypes.sizeof(NN.XbCamera),
                "d2h_bytes_per_step": W * H * 4 + 24, "ms_per_step": e2e_ms,
+               "ms_steps": [round(x, 3) for x in e2e_all] if e2e_all else None,
                "api": "render_frame() -> numpy Frame" if world == 1 else "TiledRenderer.render + D2H of the image"}
 
     # ---- roofline of the dominant kernel (k_render): algorithmic bytes / kernel time
