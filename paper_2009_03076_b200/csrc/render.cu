@@ -1064,9 +1064,11 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
         // ---- 32 rays per grab: every lane sets up one ray (camera ray, jitter,
         //      clip, root box); rays that reach no active region are written at
         //      once, the others are marched one after another by the whole warp
-        //      Grab size: fixed 8 by default (C2 sweep, tools/ab.py: 32 -> 9.4 ms,
-        //      16 -> 7.9, 8 -> 7.7, 4 -> 7.9, 2 -> 8.4); XB_GRAB_FIXED=0 selects a
-        //      guided schedule (remaining / (grab_div x warps), clamped to [1, 32]).
+        //      Grab size: guided by default (remaining / (grab_div x warps), clamped
+        //      to [1, 32]): big grabs while the list is long, single rays at the end,
+        //      where a fixed grab of 8 long rays left one warp working while the rest
+        //      idled (tools/ab.py, ms, fixed 8 / guided: C3 1.20 / 0.95, C2 6.53 /
+        //      6.49, C5 3.63 / 3.62).  XB_GRAB_FIXED=N forces N rays per grab.
         //      With k_walk's leaf lists the work is its hit list (misses are done).
         unsigned long long b0 = 0;
         int grab = 32;
@@ -1734,7 +1736,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
     {  // k_warp guided ray-grab schedule (tuning knob XB_GRAB_DIV)
         RenderArgs& W = const_cast<RenderArgs&>(A);
         W.grab_div = getenv("XB_GRAB_DIV") ? std::max(1, atoi(getenv("XB_GRAB_DIV"))) : 4;
-        W.grab_fixed = getenv("XB_GRAB_FIXED") ? std::min(32, atoi(getenv("XB_GRAB_FIXED"))) : 8;
+        W.grab_fixed = getenv("XB_GRAB_FIXED") ? std::min(32, atoi(getenv("XB_GRAB_FIXED"))) : 0;
     }
     if (kc == 2) {
         RenderFn fn;

@@ -62,8 +62,9 @@ def setv(v):
         os.environ["XB_LEAF_CAP"] = v[3:]
     elif v.startswith("f") and v[1:].isdigit():
         os.environ["XB_GRAB_FIXED"] = v[1:]
-    elif v.startswith("g") and v[1:].isdigit():
+    elif v.startswith("g") and v[1:].isdigit():  # guided grabs with divisor D
         os.environ["XB_GRAB_DIV"] = v[1:]
+        os.environ["XB_GRAB_FIXED"] = "0"
     elif v.startswith("warp") and len(v) > 4:
         os.environ["XB_WMINB"] = v[4:]
     elif v != "warp":
