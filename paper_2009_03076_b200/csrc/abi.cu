@@ -576,10 +576,10 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->out8 = o8.dev;
         A->outf = of.dev;
         A->outcnt = oc.dev;
-        // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter, walk counter, hits]
+        // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter, list lengths x5]
         unsigned long long* scratch = nullptr;
-        XB_CUDA(cudaMallocAsync((void**)&scratch, 8 * sizeof(unsigned long long), s));
-        XB_CUDA(cudaMemsetAsync(scratch, 0, 8 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMallocAsync((void**)&scratch, 16 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMemsetAsync(scratch, 0, 16 * sizeof(unsigned long long), s));
         A->walk_counter = scratch + 4;
         unsigned long long* dstats = (stats || count_bytes) ? scratch : nullptr;
         A->stats = dstats;
@@ -597,6 +597,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->leaves = nullptr;
         A->leaf_count = nullptr;
         A->short_list = nullptr;
+        A->long_list = nullptr;
+        A->any_list = nullptr;
         A->short_min = 0;
         A->walk_cap1 = 0;
         A->walk2_min = 0;
@@ -632,7 +634,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                 const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
                 const size_t ns1 = std::max<size_t>(n_slots, 1);
                 const size_t res_words = 1 + 3 * 48;  // render.cu kResume
-                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, ns1 * (cap + 4 + res_words) * sizeof(int32_t), s));
+                const size_t nblk = (ns1 + xb::kWalkThreads - 1) / xb::kWalkThreads;
+                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, (ns1 * (cap + 6 + res_words) + 3 * nblk) * sizeof(int32_t), s));
                 A->leaf_count = leaf_buf;
                 A->hit_list = leaf_buf + ns1;
                 // two-pass walk: pass 1 caps at 16 leaves; pass 2 continues the cap-cut walks to the
@@ -643,6 +646,10 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                 A->walk_cap1 = ec ? cap : (e1 ? std::max(1, atoi(e1)) : 16);
                 const char* e2 = getenv("XB_WALK2_MIN");
                 A->cut_list = leaf_buf + (3 + res_words + cap) * ns1;
+                A->long_list = leaf_buf + (4 + res_words + cap) * ns1;
+                A->any_list = leaf_buf + (5 + res_words + cap) * ns1;
+                A->blk_counts = leaf_buf + (6 + res_words + cap) * ns1;
+                A->cut_tau = getenv("XB_CUT_TAU") ? atoi(getenv("XB_CUT_TAU")) : 1;
                 // k_short for rays with <= 8 leaves and <= 24 estimated samples, used only when the
                 // frame has >= 1000 x SMs of them (decided on the device).  tools/ab.py, ms, forced on
                 // vs off: C3 (270K short rays) 1.56 vs 1.61, C5 (44K) 3.70 vs 3.40, C2 (57K) 6.82 vs
@@ -675,7 +682,7 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             }
             fprintf(stderr, "xb_render: %llu candidates; leaves 0:%lld 1-2:%lld 3-4:%lld 5-8:%lld 9-16:%lld "
                             "17-32:%lld 33-64:%lld >64:%lld truncated:%lld\n",
-                    (unsigned long long)xb::read_scalar(A->walk_counter + 1, s), h[0], h[1], h[2], h[3], h[4],
+                    (unsigned long long)xb::read_scalar(A->walk_counter + 3, s), h[0], h[1], h[2], h[3], h[4],
                     h[5], h[6], h[7], h[8]);
         }
         if (leaf_buf) XB_CUDA(cudaFreeAsync(leaf_buf, s));

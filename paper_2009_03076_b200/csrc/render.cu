@@ -19,7 +19,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
+
 #include "march.cuh"
+
 #include "render.cuh"
 
 namespace xb {
@@ -450,7 +452,6 @@ __device__ __forceinline__ void lattice(double ci, double co, double dt, double 
 // Many small independent walks at high occupancy replace the warp frontier's
 // narrow expansion steps (a ray's k-d subtree rarely fills 32 lanes).
 
-constexpr int kWalkThreads = 128;
 constexpr int kWalkStack = 100;  // >= 3 x (Kd4 depth <= kKdStack / 2 + 1)
 constexpr int kLeafCountMask = 0x0fffffff;
 constexpr int kLeafTruncated = 0x40000000;
@@ -504,8 +505,9 @@ __device__ __forceinline__ void save_resume(const RenderArgs& A, int64_t slot, i
     }
 }
 
-// Rays that can meet an active region (root box hit after clipping) -> flag;
-// the others get their (empty / iso-coloured) pixel here and are done.
+// Rays that can meet an active region (root box hit after clipping) -> flag
+// (hit_select lists them); the others get their (empty / iso-coloured) pixel
+// here and are done.
 __global__ void __launch_bounds__(kWalkThreads) k_classify(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (slot >= n_slots) return;
@@ -563,7 +565,7 @@ __device__ __forceinline__ void walk_leaves(const RenderArgs& A, int64_t slot, c
             if (A.wqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
                 tau += __ldg(A.wqmin + rid) * (float)(tf - tn) * spc;
                 if (tau > tau_stop) {
-                    flags = kLeafTruncated;
+                    flags = kLeafTruncated | kLeafTauStop;
                     save_resume(A, slot, kNoEntry, 0.0, 0.0, st_code, st_tn, st_tf, sp_n);
                     break;
                 }
@@ -644,15 +646,28 @@ __device__ __forceinline__ void walk_leaves(const RenderArgs& A, int64_t slot, c
     }
 }
 
+// route of a walked ray: short (complete list of <= short_leaves leaves, few
+// samples) -> k_short, the rest -> k_warp / k_iso_warp; walks cut at the
+// pass-1 cap (not by the opacity minorant) also -> k_walk2
+__device__ __forceinline__ void route_of(const RenderArgs& A, int v, bool& is_short, bool& is_long, bool& is_cut) {
+    const bool any = v != 0;
+    is_short = A.short_list && any && !(v & (kLeafTruncated | kLeafHeavy)) && (v & kLeafCountMask) <= A.short_leaves;
+    is_long = any && !is_short;
+    is_cut = A.cut_list && (v & kLeafTruncated) && (A.cut_tau || !(v & kLeafTauStop));
+}
+
 __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const SceneView& S = A.S;
-    const int64_t n_cand = (int64_t)A.walk_counter[1];
+    const int64_t n_cand = (int64_t)A.walk_counter[3];
     // Pass 1 lists at most walk_cap1 leaves per ray: a few very long walks (latency
     // chains of node loads) would otherwise set the kernel's length; k_walk2
     // continues the cap-truncated walks when there are many of them.
     const int cap = A.walk_cap1;
-    for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < n_cand;
-         ci += (int64_t)gridDim.x * blockDim.x) {
+    if (blockIdx.x * (int64_t)blockDim.x >= n_cand) return;
+    bool is_short = false, is_long = false, is_cut = false;
+    {
+        const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        if (ci >= n_cand) goto route;
         const int64_t slot = A.hit_list[ci];
         int count = 0, flags = 0;
         const SlotPix spx = slot_pixel(A, slot);
@@ -680,6 +695,77 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
         } else {
             A.leaf_count[slot] = 0;
         }
+        route_of(A, count | flags, is_short, is_long, is_cut);
+    }
+route:
+    // per-block route counts for k_route (block resources are held until the
+    // slowest walk of the block ends anyway, so the barrier costs nothing)
+    const int ns = __syncthreads_count(is_short), nl = __syncthreads_count(is_long),
+              nc = __syncthreads_count(is_cut);
+    if (threadIdx.x == 0) {
+        A.blk_counts[3 * blockIdx.x] = ns;
+        A.blk_counts[3 * blockIdx.x + 1] = nl;
+        A.blk_counts[3 * blockIdx.x + 2] = nc;
+    }
+    (void)n_slots;
+}
+
+// After k_walk: the short / long / cut lists in hit-list (screen) order.  Block b
+// takes the hits of k_walk's block b, sums the route counts of the blocks
+// before it, ranks its rays with ballots and writes them; the last block
+// publishes the list lengths.  (Order matters for speed, not results: lists in
+// walk-completion order cost C3 16 %, C2 8 % in k_warp / k_short locality.)
+__global__ void __launch_bounds__(kWalkThreads) k_route(const __grid_constant__ RenderArgs A, int64_t n_slots) {
+    __shared__ int s_sum[3][kWalkThreads / 32];
+    const int64_t n_cand = (int64_t)A.walk_counter[3];
+    const int64_t nb = (n_cand + blockDim.x - 1) / blockDim.x;
+    if ((int64_t)blockIdx.x >= nb) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int p0 = 0, p1 = 0, p2 = 0;  // route counts of the blocks before this one
+    for (int64_t j = threadIdx.x; j < (int64_t)blockIdx.x; j += blockDim.x) {
+        p0 += A.blk_counts[3 * j];
+        p1 += A.blk_counts[3 * j + 1];
+        p2 += A.blk_counts[3 * j + 2];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+        p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+        p2 += __shfl_xor_sync(0xffffffffu, p2, o);
+    }
+    const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool is_short = false, is_long = false, is_cut = false;
+    int64_t slot = 0;
+    if (ci < n_cand) {
+        slot = A.hit_list[ci];
+        route_of(A, A.leaf_count[slot], is_short, is_long, is_cut);
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned ms = __ballot_sync(0xffffffffu, is_short), ml = __ballot_sync(0xffffffffu, is_long),
+                   mc = __ballot_sync(0xffffffffu, is_cut);
+    __shared__ int s_w[3][kWalkThreads / 32];
+    if (lane == 0) {
+        s_sum[0][wid] = p0; s_sum[1][wid] = p1; s_sum[2][wid] = p2;
+        s_w[0][wid] = __popc(ms); s_w[1][wid] = __popc(ml); s_w[2][wid] = __popc(mc);
+    }
+    __syncthreads();
+    int b0 = 0, b1 = 0, b2 = 0, w0 = 0, w1 = 0, w2 = 0;
+#pragma unroll
+    for (int w = 0; w < kWalkThreads / 32; w++) {
+        b0 += s_sum[0][w]; b1 += s_sum[1][w]; b2 += s_sum[2][w];
+        if (w < wid) { w0 += s_w[0][w]; w1 += s_w[1][w]; w2 += s_w[2][w]; }
+    }
+    if (is_short) A.short_list[b0 + w0 + __popc(ms & lt)] = (int32_t)slot;
+    if (is_long) A.long_list[b1 + w1 + __popc(ml & lt)] = (int32_t)slot;
+    if (is_cut) A.cut_list[b2 + w2 + __popc(mc & lt)] = (int32_t)slot;
+    if (A.any_list && (is_short || is_long))  // short + long merged, in hit order
+        A.any_list[b0 + b1 + w0 + w1 + __popc((ms | ml) & lt)] = (int32_t)slot;
+    if ((int64_t)blockIdx.x == nb - 1 && threadIdx.x == 0) {
+        int t0 = b0, t1 = b1, t2 = b2;
+        for (int w = 0; w < kWalkThreads / 32; w++) { t0 += s_w[0][w]; t1 += s_w[1][w]; t2 += s_w[2][w]; }
+        A.walk_counter[0] = (unsigned long long)t0;
+        A.walk_counter[1] = (unsigned long long)t1;
+        A.walk_counter[2] = (unsigned long long)t2;
+        A.walk_counter[4] = (unsigned long long)(t0 + t1);
     }
     (void)n_slots;
 }
@@ -688,13 +774,6 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ R
 // opacity minorant) up to leaf_cap, from their saved ordered remainder — only
 // when there are at least walk2_min of them (decided on the device): many long
 // rays (C2, C5) are cheaper here than in k_warp's frontier; a few (C3) are not.
-struct IsCapCut {
-    const int32_t* c;
-    __device__ __forceinline__ bool operator()(const int32_t i) const {
-        const int v = c[i];
-        return (v & kLeafTruncated) && !(v & kLeafTauStop);
-    }
-};
 
 __global__ void __launch_bounds__(kWalkThreads) k_walk2(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const int64_t n_cut = (int64_t)A.walk_counter[2];
@@ -737,7 +816,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_iso_march(const __grid_constan
     const int64_t n_cand = (int64_t)A.walk_counter[1];
     const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (ci >= n_cand) return;
-    const int64_t slot = A.hit_list[ci];
+    const int64_t slot = A.long_list[ci];
     const SlotPix sp = slot_pixel(A, slot);
     Ray r;
     pixel_ray(A, sp.x, sp.y, r);
@@ -775,7 +854,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant
         if (lane == 0) c = atomicAdd(A.work_counter, 1ull);
         c = __shfl_sync(FULL, c, 0);
         if ((int64_t)c >= n_cand) break;
-        const int64_t slot = A.hit_list[c];
+        const int64_t slot = A.long_list[c];
         const SlotPix sp = slot_pixel(A, slot);
         Ray r;
         pixel_ray(A, sp.x, sp.y, r);
@@ -894,35 +973,6 @@ __global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant
     }
     (void)n_slots;
 }
-
-// hit rays (leaf_count != 0) -> k_walk's work list, in slot (screen-tile) order
-struct HasLeaves {
-    const int32_t* c;
-    __device__ __forceinline__ bool operator()(const int32_t i) const { return c[i] != 0; }
-};
-
-// after k_walk: short rays (complete lists of <= kShortLeaves leaves) go to
-// k_short, the rest (long or truncated) to k_warp
-struct IsShort {
-    const int32_t* c;
-    int max_leaves;
-    __device__ __forceinline__ bool operator()(const int32_t i) const {
-        const int v = c[i];
-        return v != 0 && !(v & (kLeafTruncated | kLeafHeavy)) && (v & kLeafCountMask) <= max_leaves;
-    }
-};
-struct IsLong {  // long rays, plus the short ones when too few for k_short to pay (n_short < short_min)
-    const int32_t* c;
-    const unsigned long long* n_short;
-    long long short_min;
-    int max_leaves;
-    __device__ __forceinline__ bool operator()(const int32_t i) const {
-        const int v = c[i];
-        if (v == 0) return false;
-        const bool is_long = (v & (kLeafTruncated | kLeafHeavy)) || (v & kLeafCountMask) > max_leaves;
-        return is_long || (long long)*n_short < short_min;
-    }
-};
 
 // k_short: one thread per short ray (C3: 87 % of the rays that meet an active
 // region list 1-8 leaves and take a handful of samples, which would leave most
@@ -1058,7 +1108,10 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     const SceneView& S = A.S;
     const double early = A.M.early;
     unsigned long long tot_reg = 0, tot_smp = 0, tot_bytes = 0;
-    const int64_t n_work = A.leaves ? (int64_t)A.walk_counter[1] : n_slots;
+    // work: the long list, or long + short merged when the short rays are too few for k_short
+    const bool merged = A.leaves && (!A.short_list || (int64_t)A.walk_counter[0] < A.short_min);
+    const int32_t* __restrict__ work = merged ? A.any_list : A.long_list;
+    const int64_t n_work = !A.leaves ? n_slots : (int64_t)A.walk_counter[merged ? 4 : 1];
 
     for (;;) {
         // ---- 32 rays per grab: every lane sets up one ray (camera ray, jitter,
@@ -1083,7 +1136,8 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
         grab = __shfl_sync(FULL, grab, 0);
         if ((int64_t)b0 >= n_work) break;
         const bool my_in = lane < grab && (int64_t)b0 + lane < n_work;
-        const int64_t my_slot = A.leaves ? (my_in ? (int64_t)A.hit_list[b0 + lane] : 0) : (int64_t)b0 + lane;
+        const int64_t wi = (int64_t)b0 + lane;
+        const int64_t my_slot = !A.leaves ? wi : (my_in ? (int64_t)work[wi] : 0);
         SlotPix msp = slot_pixel(A, my_slot);
         msp.live = msp.live && my_in;
         Ray mr;
@@ -1681,14 +1735,24 @@ static int kernel_choice() {
 }
 
 // slots i in [0, n) with pred(i), in order -> out, count -> *n_out (device)
-template <class Pred>
-static void select_flagged(int32_t* out, unsigned long long* n_out, Pred pred, int64_t n, cudaStream_t s) {
+// flagged rays (leaf_count != 0 after k_classify) -> hit_list in slot (screen)
+// order, length -> walk_counter[3].  Screen order keeps neighbouring rays
+// together in k_walk / k_warp: a list in arrival order (warp-aggregated atomics
+// in k_classify) cost C2 / C3 5-7 %.
+struct HasLeaves {
+    const int32_t* c;
+    __device__ __forceinline__ bool operator()(const int32_t i) const { return c[i] != 0; }
+};
+
+static void hit_select(const RenderArgs& A, int64_t n_slots, cudaStream_t s) {
     size_t tb = 0;
     cub::CountingInputIterator<int32_t> it(0);
-    XB_CUDA(cub::DeviceSelect::If(nullptr, tb, it, out, n_out, (int)n, pred, s));
+    XB_CUDA(cub::DeviceSelect::If(nullptr, tb, it, A.hit_list, A.walk_counter + 3, (int)n_slots,
+                                  HasLeaves{A.leaf_count}, s));
     void* tmp = nullptr;
     XB_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 16), s));
-    XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, out, n_out, (int)n, pred, s));
+    XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.hit_list, A.walk_counter + 3, (int)n_slots,
+                                  HasLeaves{A.leaf_count}, s));
     XB_CUDA(cudaFreeAsync(tmp, s));
 }
 
@@ -1712,11 +1776,14 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         Ai->short_list = nullptr;
         Ai->walk_cap1 = std::min(A.leaf_cap, 16);
         void* iargs[] = {(void*)Ai, (void*)&n_slots};
+        Ai->cut_list = nullptr;
         XB_CUDA(cudaLaunchKernel((const void*)k_classify, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
                                  iargs, 0, s));
-        select_flagged(A.hit_list, A.walk_counter + 1, HasLeaves{A.leaf_count}, n_slots, s);
+        hit_select(*Ai, n_slots, s);
         XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads), iargs,
                                  0, s));
+        XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
+                                 iargs, 0, s));
         if (getenv("XB_ISO_LANE")) {  // A/B: one thread per iso ray
             const void* mf = count ? (const void*)k_iso_march<true> : (const void*)k_iso_march<false>;
             XB_CUDA(cudaLaunchKernel(mf, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads), iargs, 0, s));
@@ -1731,6 +1798,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             // k_warp's ray counter is shared: reset it for the volume phase
             XB_CUDA(cudaMemsetAsync(A.work_counter, 0, sizeof(unsigned long long), s));
         }
+        XB_CUDA(cudaMemsetAsync(A.walk_counter, 0, 5 * sizeof(unsigned long long), s));  // volume phase lists
     }
     const int kc = A.M.use_tree ? 2 : kernel_choice();  // cell location: the one-thread-per-pixel kernel
     {  // k_warp guided ray-grab schedule (tuning knob XB_GRAB_DIV)
@@ -1769,28 +1837,17 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             void* wargs[] = {(void*)&A, (void*)&n_slots};
             XB_CUDA(cudaLaunchKernel((const void*)k_classify, dim3(grid_for(n_slots, kWalkThreads)),
                                      dim3(kWalkThreads), wargs, 0, s));
-            size_t tb = 0;
-            cub::CountingInputIterator<int32_t> it(0);
-            XB_CUDA(cub::DeviceSelect::If(nullptr, tb, it, A.hit_list, A.walk_counter + 1, (int)n_slots,
-                                          HasLeaves{A.leaf_count}, s));
-            void* tmp = nullptr;
-            XB_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 16), s));
-            XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.hit_list, A.walk_counter + 1, (int)n_slots,
-                                          HasLeaves{A.leaf_count}, s));
-            // one thread per candidate (blocks past the device-side count exit at once)
+            hit_select(A, n_slots, s);
+            // one thread per candidate (blocks past the device-side count exit at once), then
+            // k_route builds the short / long / cut lists
             XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
                                      wargs, 0, s));
-            if (A.cut_list && A.walk_cap1 < A.leaf_cap) {  // pass 2 over the cap-cut walks
-                XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.cut_list, A.walk_counter + 2, (int)n_slots,
-                                              IsCapCut{A.leaf_count}, s));
+            XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
+                                     wargs, 0, s));
+            if (A.cut_list && A.walk_cap1 < A.leaf_cap)  // pass 2 over the cap-cut walks
                 XB_CUDA(cudaLaunchKernel((const void*)k_walk2, dim3(grid_for(n_slots, kWalkThreads)),
                                          dim3(kWalkThreads), wargs, 0, s));
-            }
-            if (A.short_list) {  // short rays -> k_short, long ones -> k_warp (hit_list, count walk_counter[1])
-                XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.short_list, A.walk_counter, (int)n_slots,
-                                              IsShort{A.leaf_count, A.short_leaves}, s));
-                XB_CUDA(cub::DeviceSelect::If(tmp, tb, it, A.hit_list, A.walk_counter + 1, (int)n_slots,
-                                              IsLong{A.leaf_count, A.walk_counter, A.short_min, A.short_leaves}, s));
+            if (A.short_list) {  // short rays -> k_short (when >= short_min of them), long ones -> k_warp
                 using ShortFn = void (*)(RenderArgs, int64_t);
                 ShortFn sf;
                 if (g == 0) sf = iso ? (ShortFn)k_short<0, true, false> : (ShortFn)k_short<0, false, false>;
@@ -1804,7 +1861,6 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
                 XB_CUDA(cudaLaunchKernel((const void*)sf, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
                                          wargs, 0, s));
             }
-            XB_CUDA(cudaFreeAsync(tmp, s));
         }
         if (g == 0) fn = iso ? warp_fn<0, true>(count) : warp_fn<0, false>(count);
         else if (g == 1) fn = iso ? warp_fn<1, true>(count) : warp_fn<1, false>(count);

@@ -11,6 +11,8 @@ constexpr int kFrameMinBlocks = 4;      // 128 regs/thread -> 16 warps/SM (more 
 
 // Passed by value as a __grid_constant__ kernel parameter (~8.6 KB < 32 KB):
 // the call needs no device allocation, so concurrent renders are reentrant.
+constexpr int kWalkThreads = 128;  // k_classify / k_walk / k_route / k_short block size
+
 struct RenderArgs {
     SceneView S;
     const uint8_t* vflags;  // per k-d node: subtree holds an active volume region
@@ -43,8 +45,12 @@ struct RenderArgs {
     long long walk_budget;             // k_walk: clock cycles per walk before it hands over (0 = none)
     int32_t* resume;                   // per slot: k_walk's ordered remainder when truncated (1 + 3 x kResume words)
     const float* vqmin;                // per region opacity minorant (k_walk early stop), may be NULL
-    unsigned long long* walk_counter;  // k_walk slot counter, then the hit-list length
-    int32_t* hit_list;                 // candidate rays (k_walk's work), then the long rays (k_warp's)
+    unsigned long long* walk_counter;  // list lengths: [0] short, [1] long, [2] cut, [3] hit, [4] any
+    int32_t* hit_list;                 // candidate rays (k_walk's work), appended by k_classify
+    int32_t* long_list;                // rays for k_warp / k_iso_warp (k_route, in hit-list order)
+    int32_t* any_list;                 // long + short rays, merged (k_warp's work when k_short is off)
+    int cut_tau;                       // k_walk2 also continues walks stopped by the opacity minorant
+    int32_t* blk_counts;               // k_walk -> k_route: short / long / cut rays per k_walk block
     int32_t* short_list;               // rays with a complete list of <= 8 leaves (k_short's work), or NULL
     long long short_min;               // k_short runs only for at least this many short rays (else k_warp takes them)
     int short_leaves;                  // short ray: complete list of <= short_leaves leaves ...

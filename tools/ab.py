@@ -33,7 +33,7 @@ def setv(v):
     for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU",
               "XB_TRAVERSAL", "XB_CAP_DIV", "XB_WALK_BUDGET", "XB_SHORT", "XB_SHORT_LEAVES", "XB_SHORT_SAMPLES"):
         os.environ.pop(k, None)
-    for k in ("XB_WALK_CAP1", "XB_WALK2_MIN", "XB_WALK_CAP2"):
+    for k in ("XB_WALK_CAP1", "XB_WALK2_MIN", "XB_WALK_CAP2", "XB_CUT_TAU"):
         os.environ.pop(k, None)
     if v.startswith("w2_"):  # w2_X_Y: pass-1 cap X, pass-2 cap Y
         os.environ["XB_WALK_CAP1"], os.environ["XB_WALK_CAP2"] = v[3:].split("_")
@@ -43,6 +43,9 @@ def setv(v):
         return
     if v.startswith("sl") and "_" in v:  # slL_S: short-ray thresholds
         os.environ["XB_SHORT_LEAVES"], os.environ["XB_SHORT_SAMPLES"] = v[2:].split("_")
+        return
+    if v == "cutnotau":
+        os.environ["XB_CUT_TAU"] = "0"
         return
     if v == "short":
         os.environ["XB_SHORT"] = "1"

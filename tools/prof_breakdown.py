@@ -40,14 +40,14 @@ sc = find(src, "inclusive scan of the front-to-back", kw)
 tr = find(src, "// ================= traversal", kw)
 co = find(src, "// ---- consume leading leaves", kw)
 ex = find(src, "// ---- expansion step", kw)
-en = find(src, "if (lane == 0) {", ex)
+en = find(src, "if (lane == 0) {", co)
 R = lambda x, y: (lambda r: r[0] == "render.cu" and x <= r[1] < y)
 agg("ray setup", R(kw, c0))
 agg("chunk map + eval", R(c0, sc))
 agg("scan + queue drop", R(sc, tr))
-agg("frontier refill", R(tr, co))
-agg("consume leaves", R(co, ex))
-agg("expand", R(ex, en))
+agg("list / frontier refill", R(tr, ex))
+agg("expand", R(ex, co))
+agg("consume leaves", R(co, en))
 agg("pixel write", R(en, en + 40))
 agg("render.cu helpers", lambda r: r[0] == "render.cu" and not (kw <= r[1] < en + 40))
 g0 = find(msrc, "void gather_shade(")
