@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <vector>
 #include "../../include/exabricks.h"
 #include "accel.cuh"
@@ -27,6 +28,11 @@ struct xb_model {
 struct xb_regions {
     xb::DevRegions r;
     int64_t model_bricks = 0;
+    // brick records in region-list order for the frame gather (built on first render)
+    mutable std::mutex rb_mu;
+    mutable xb::DevBuf<int4> rb_a;
+    mutable xb::DevBuf<uint32_t> rb_m;
+    mutable bool rb_ok = false;
 };
 struct xb_active {
     xb::DevActive a;
@@ -86,6 +92,31 @@ void keep_pool(int device) {
     done[device] = true;
 }
 
+__global__ void k_region_bricks(const int32_t* __restrict__ ids, int64_t n, const int4* __restrict__ ba,
+                                const uint32_t* __restrict__ bm, int4* __restrict__ ra, uint32_t* __restrict__ rm) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int b = ids[i];
+    ra[i] = ba[b];
+    rm[i] = bm[b];
+}
+
+void ensure_region_bricks(const xb_model* m, const xb_regions* r) {
+    std::lock_guard<std::mutex> g(r->rb_mu);
+    if (r->rb_ok) return;
+    const int64_t n = std::max<int64_t>(r->r.n_ids, 1);
+    r->rb_a.alloc(n);
+    r->rb_m.alloc(n);
+    if (r->r.n_ids > 0) {
+        OwnedStream st;
+        k_region_bricks<<<(unsigned)((r->r.n_ids + 255) / 256), 256, 0, st.s>>>(
+            r->r.ids.p, r->r.n_ids, m->m.brick_a.p, m->m.brick_m.p, r->rb_a.p, r->rb_m.p);
+        XB_CUDA(cudaGetLastError());
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    }
+    r->rb_ok = true;
+}
+
 xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     XB_CHECK(m && r, XB_ERR_ARG, "null model or regions");
     XB_CHECK(r->model_bricks == m->m.n_bricks, XB_ERR_ARG, "regions were built for a different model");
@@ -98,6 +129,9 @@ xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     S.vals = m->m.vals.p + (size_t)field * (size_t)m->m.n_cells;
     S.rec = r->r.rec.p;
     S.rids = r->r.ids.p;
+    ensure_region_bricks(m, r);
+    S.rb_a = r->rb_a.p;
+    S.rb_m = r->rb_m.p;
     S.kd = r->r.kd.p;
     S.kd4 = r->r.kd4.p;
     for (int a = 0; a < 3; a++) {

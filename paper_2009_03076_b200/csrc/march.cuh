@@ -93,6 +93,10 @@ struct SceneView {
     const float* __restrict__ vals;
     const RegionRec* __restrict__ rec;
     const int32_t* __restrict__ rids;
+    // brick records in region-list order (rb_a[i] = brick_a[rids[i]], same for
+    // rb_m): the frame gather reads a region's bricks without the id hop
+    const int4* __restrict__ rb_a;
+    const uint32_t* __restrict__ rb_m;
     const KdNode* __restrict__ kd;
     const Kd4Node* __restrict__ kd4;
     int32_t root_lo[3], root_hi[3];
@@ -587,9 +591,8 @@ struct ShadeAcc {
 
 // one brick of the frame gather: adds brick b's window cells to A
 template <bool GRAD>
-__device__ __forceinline__ void brick_step(const SceneView& S, int b, double px, double py, double pz, ShadeAcc& A) {
-    const int4 ba = __ldg(S.brick_a + b);
-    const uint32_t bm = __ldg(S.brick_m + b);
+__device__ __forceinline__ void brick_step(const SceneView& S, const int4 ba, const uint32_t bm, double px, double py,
+                                           double pz, ShadeAcc& A) {
     const int lev = bm & 31;
     const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
     const double w = pow2(lev), iw_d = pow2(-lev);
@@ -692,12 +695,15 @@ __device__ __forceinline__ void brick_step(const SceneView& S, int b, double px,
     }
 }
 
+// the frame gather over region-list entries [off, off + nids) (S.rb_a / rb_m)
 template <bool GRAD>
-__device__ __forceinline__ void gather_shade(const SceneView& S, const int32_t* __restrict__ ids, int nids, double px,
-                                             double py, double pz, FastAccum& F) {
+__device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, int nids, double px, double py,
+                                             double pz, FastAccum& F) {
     ShadeAcc A;
     A.clear();
-    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, __ldg(ids + t), px, py, pz, A);
+    const int4* __restrict__ ra = S.rb_a + off;
+    const uint32_t* __restrict__ rm = S.rb_m + off;
+    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, __ldg(ra + t), __ldg(rm + t), px, py, pz, A);
     F.num = A.num;
     F.den = A.den;
     F.n_nz = A.n_nz;

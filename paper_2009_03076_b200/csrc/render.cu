@@ -1028,7 +1028,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_short(const __grid_constant__ 
                 nsmp++;
                 const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1], pz = r.o[2] + mid * r.d[2];
                 FastAccum F;
-                gather_shade<GRAD == 1>(S, ids, nids, px, py, pz, F);
+                gather_shade<GRAD == 1>(S, (int64_t)rr.ids_begin, nids, px, py, pz, F);
                 if (COUNT) my_bytes += 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
                 if (F.den > kEpsWeight) {
                     const double v = F.num / F.den;
@@ -1267,7 +1267,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         if (kFlatGather) {
                             gather_chunk<GRAD == 1>(S, act, sq.ids, nids, px, py, pz, s_part[wid], lane, F);
                         } else if (act) {
-                            gather_shade<GRAD == 1>(S, S.rids + sq.ids, nids, px, py, pz, F);
+                            gather_shade<GRAD == 1>(S, (int64_t)sq.ids, nids, px, py, pz, F);
                         }
                         if (act) {
                             if (COUNT) my_bytes = 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
