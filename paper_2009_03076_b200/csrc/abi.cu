@@ -618,6 +618,7 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         unsigned long long* dstats = (stats || count_bytes) ? scratch : nullptr;
         A->stats = dstats;
         A->work_counter = scratch + 3;
+        A->dbg = getenv("XB_DEBUG_CHUNKS") ? scratch + 9 : nullptr;  // [9, 16)
         double* iso_buf = nullptr;
         if (A->M.iso_on) {
             const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
@@ -718,6 +719,15 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
                             "17-32:%lld 33-64:%lld >64:%lld truncated:%lld\n",
                     (unsigned long long)xb::read_scalar(A->walk_counter + 3, s), h[0], h[1], h[2], h[3], h[4],
                     h[5], h[6], h[7], h[8]);
+        }
+        if (A->dbg) {
+            unsigned long long d[7];
+            XB_CUDA(cudaMemcpyAsync(d, A->dbg, sizeof d, cudaMemcpyDeviceToHost, s));
+            XB_CUDA(cudaStreamSynchronize(s));
+            fprintf(stderr, "xb_render: k_warp %llu rays, %llu samples, %llu regions, %llu chunks, %.1f lanes/chunk, "
+                            "%.2f bricks/sample, %.2f max bricks/chunk\n",
+                    d[2], d[3], d[4], d[0], d[0] ? (double)d[1] / (double)d[0] : 0.0,
+                    d[1] ? (double)d[5] / (double)d[1] : 0.0, d[0] ? (double)d[6] / (double)d[0] : 0.0);
         }
         if (leaf_buf) XB_CUDA(cudaFreeAsync(leaf_buf, s));
         if (iso_buf) XB_CUDA(cudaFreeAsync(iso_buf, s));

@@ -731,14 +731,13 @@ struct BrickPart {
 static_assert(sizeof(BrickPart) == 64, "BrickPart is 64 bytes");
 
 template <bool GRAD>
-__device__ __forceinline__ void brick_part(const SceneView& S, int b, double px, double py, double pz, BrickPart& P) {
+__device__ __forceinline__ void brick_part(const SceneView& S, const int4 ba, const uint32_t bm, double px, double py,
+                                           double pz, BrickPart& P) {
     P.num = 0.0;
     P.den = 0.0;
     P.nnz = 0;
     P.fden = P.gnum = P.dn0 = P.dn1 = P.dn2 = P.dd0 = P.dd1 = P.dd2 = 0.f;
     P.v0 = 0.f;
-    const int4 ba = __ldg(S.brick_a + b);
-    const uint32_t bm = __ldg(S.brick_m + b);
     const int lev = bm & 31;
     const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
     const double w = pow2(lev), iw_d = pow2(-lev);
@@ -856,7 +855,8 @@ __device__ __forceinline__ void gather_chunk(const SceneView& S, bool act, int i
         const int qe = __shfl_sync(FULL, Qe, j), qoff = __shfl_sync(FULL, ids_off, j);
         BrickPart P;
         if (q < I) {
-            brick_part<GRAD>(S, __ldg(S.rids + qoff + (q - qe)), qx, qy, qz, P);
+            const int64_t e = (int64_t)qoff + (q - qe);
+            brick_part<GRAD>(S, __ldg(S.rb_a + e), __ldg(S.rb_m + e), qx, qy, qz, P);
         } else {
             P.num = P.den = 0.0;
             P.nnz = 0;

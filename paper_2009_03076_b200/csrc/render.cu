@@ -362,9 +362,14 @@ constexpr int kWarpMinBlocks = 4;
 constexpr int kWarpsPerBlock = kWarpThreads / 32;
 constexpr int kWarpStack = 256;  // spilled frontier entries per warp
 constexpr int kRaysPerGrab = 8;  // rays taken per work-counter atomic
-// (sample, brick)-flattened chunk gather (march.cuh:gather_chunk): measured
-// slower on C2 (12.3 vs 10.1 ms) — the per-owner accumulation loop diverges
-// as much as the per-sample brick loop it replaces; kept for A/B
+// (sample, brick)-flattened chunk gather (march.cuh:gather_chunk).  The
+// per-sample brick loop runs max(nids) iterations per chunk, so about half of
+// its lane-brick slots idle (XB_DEBUG_CHUNKS: C3 5.1 bricks/sample vs 7.2 per
+// chunk, C2 2.4 vs 4.3, C5 1.6 vs 3.1), yet the flattened form — fewer rounds,
+// but partials through shared memory, a warp barrier per round and the
+// per-owner combine loop — measured slower every time: C2 12.3 vs 10.1 ms
+// (first pipeline), C3 1.21 vs 0.92 and C2 8.74 vs 6.31 (walk lists).  Kept
+// for A/B.
 constexpr bool kFlatGather = false;
 
 struct SegQ {       // one visited region of the segment queue
@@ -1098,7 +1103,8 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     __shared__ SegQ s_q[kWarpsPerBlock][32];
     __shared__ RayAxes s_ray[kWarpsPerBlock];
     __shared__ RaySetup s_setup[kWarpsPerBlock][32];
-    __shared__ BrickPart s_part[kFlatGather ? kWarpsPerBlock : 1][32];
+    extern __shared__ BrickPart s_part_dyn[];  // kFlatGather: 32 per warp (dynamic: static smem is at 42 KB)
+    BrickPart* s_part = s_part_dyn + (threadIdx.x >> 5) * 32;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
     __syncthreads();
     const unsigned FULL = 0xffffffffu;
@@ -1236,6 +1242,10 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                     if (pending >= 32 || (!walk && pending > 0)) {
                         // ================= one chunk of (up to) 32 samples
                         const int m = min(32, pending);
+                        if (A.dbg && lane == 0) {
+                            atomicAdd(A.dbg, 1ull);
+                            atomicAdd(A.dbg + 1, (unsigned long long)m);
+                        }
                         const int s = h0 + lane;
                         const bool act = lane < m;
                         int sg = 0;  // segment of sample s: #{i : q_P[i] <= s}
@@ -1263,9 +1273,20 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             py = r.o[1] + mid * r.d[1];
                             pz = r.o[2] + mid * r.d[2];
                         }
+                        if (A.dbg) {
+                            int nn = act ? nids : 0, mx = nn;
+                            for (int o = 16; o > 0; o >>= 1) {
+                                nn += __shfl_xor_sync(FULL, nn, o);
+                                mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+                            }
+                            if (lane == 0) {
+                                atomicAdd(A.dbg + 5, (unsigned long long)nn);
+                                atomicAdd(A.dbg + 6, (unsigned long long)mx);
+                            }
+                        }
                         FastAccum F;
                         if (kFlatGather) {
-                            gather_chunk<GRAD == 1>(S, act, sq.ids, nids, px, py, pz, s_part[wid], lane, F);
+                            gather_chunk<GRAD == 1>(S, act, sq.ids, nids, px, py, pz, s_part, lane, F);
                         } else if (act) {
                             gather_shade<GRAD == 1>(S, (int64_t)sq.ids, nids, px, py, pz, F);
                         }
@@ -1633,6 +1654,11 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                     }
                 }
                 write_pixel(A, out_px, acc, nreg, nsmp);
+                if (A.dbg) {
+                    atomicAdd(A.dbg + 2, 1ull);
+                    atomicAdd(A.dbg + 3, (unsigned long long)nsmp);
+                    atomicAdd(A.dbg + 4, (unsigned long long)nreg);
+                }
                 tot_reg += nreg;
                 tot_smp += nsmp;
             }
@@ -1875,12 +1901,17 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
     int dev = 0, sms = 0, per_sm = 0;
     XB_CUDA(cudaGetDevice(&dev));
     XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, 0));
+    size_t dyn = 0;
+    if (kc == 0 && kFlatGather) {
+        dyn = kWarpsPerBlock * 32 * sizeof(BrickPart);
+        XB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    }
+    XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, dyn));
     const int64_t per_thread = kc == 1 ? 1 : 32;  // k_warp: one ray per warp at a time
     const int64_t want = (n_slots * per_thread + threads - 1) / threads;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), want));
     void* args[] = {(void*)&A, (void*)&n_slots};
-    XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(threads), args, 0, s));
+    XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(threads), args, dyn, s));
 }
 
 // ---------------------------------------------------------------------------

@@ -29,12 +29,19 @@ stream = torch.cuda.current_stream()
 
 
 def setv(v):
+    for k in [k for k in os.environ if k.startswith("XB_") and k != "XB_LIB"]:
+        os.environ.pop(k)
     """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N) | gD (guided grab divisor D)"""
     for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU",
               "XB_TRAVERSAL", "XB_CAP_DIV", "XB_WALK_BUDGET", "XB_SHORT", "XB_SHORT_LEAVES", "XB_SHORT_SAMPLES"):
         os.environ.pop(k, None)
     for k in ("XB_WALK_CAP1", "XB_WALK2_MIN", "XB_WALK_CAP2", "XB_CUT_TAU"):
         os.environ.pop(k, None)
+    if v.startswith("e:"):  # e:K=V+K2=V2: arbitrary XB_* settings
+        for kv in v[2:].split("+"):
+            k, val = kv.split("=")
+            os.environ[k] = val
+        return
     if v.startswith("w2_"):  # w2_X_Y: pass-1 cap X, pass-2 cap Y
         os.environ["XB_WALK_CAP1"], os.environ["XB_WALK_CAP2"] = v[3:].split("_")
         return
