@@ -629,10 +629,11 @@ __device__ __forceinline__ void brick_step(const SceneView& S, const int4 ba, co
     const int r00 = nx * (ya + ny * za), r01 = nx * (yb + ny * za), r10 = nx * (ya + ny * zb),
               r11 = nx * (yb + ny * zb);
     float vv[2][2][2];  // [dz][dy][dx]
-    vv[0][0][0] = __ldg(base + r00 + xa); vv[0][0][1] = __ldg(base + r00 + xb);
-    vv[0][1][0] = __ldg(base + r01 + xa); vv[0][1][1] = __ldg(base + r01 + xb);
-    vv[1][0][0] = __ldg(base + r10 + xa); vv[1][0][1] = __ldg(base + r10 + xb);
-    vv[1][1][0] = __ldg(base + r11 + xa); vv[1][1][1] = __ldg(base + r11 + xb);
+    // 32-bit in-brick offsets: one 64-bit base, then a scaled add per load
+    vv[0][0][0] = __ldg(base + (r00 + xa)); vv[0][0][1] = __ldg(base + (r00 + xb));
+    vv[0][1][0] = __ldg(base + (r01 + xa)); vv[0][1][1] = __ldg(base + (r01 + xb));
+    vv[1][0][0] = __ldg(base + (r10 + xa)); vv[1][0][1] = __ldg(base + (r10 + xb));
+    vv[1][1][0] = __ldg(base + (r11 + xa)); vv[1][1][1] = __ldg(base + (r11 + xb));
 #if XB_EXACT_VALUE
     const double hxy00 = hx0 * hy0, hxy01 = hx1 * hy0, hxy10 = hx0 * hy1, hxy11 = hx1 * hy1;  // [dy][dx]
     const double hzz[2] = {hz0, hz1};
