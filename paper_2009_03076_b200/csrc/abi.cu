@@ -610,15 +610,18 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->out8 = o8.dev;
         A->outf = of.dev;
         A->outcnt = oc.dev;
-        // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter, list lengths x5]
+        // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter, list lengths x5,
+        // debug counters x7, short-ray grab counter]
         unsigned long long* scratch = nullptr;
-        XB_CUDA(cudaMallocAsync((void**)&scratch, 16 * sizeof(unsigned long long), s));
-        XB_CUDA(cudaMemsetAsync(scratch, 0, 16 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMallocAsync((void**)&scratch, 24 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMemsetAsync(scratch, 0, 24 * sizeof(unsigned long long), s));
         A->walk_counter = scratch + 4;
         unsigned long long* dstats = (stats || count_bytes) ? scratch : nullptr;
         A->stats = dstats;
         A->work_counter = scratch + 3;
         A->dbg = getenv("XB_DEBUG_CHUNKS") ? scratch + 9 : nullptr;  // [9, 16)
+        A->short_counter = scratch + 16;
+        A->fuse_short = getenv("XB_FUSE_SHORT") ? atoi(getenv("XB_FUSE_SHORT")) : 1;
         double* iso_buf = nullptr;
         if (A->M.iso_on) {
             const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;

@@ -985,6 +985,100 @@ __global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant
 // _volume_ray loop over its leaf list verbatim (R/render.py:380-453: exact
 // restart chain, lattice, sequential front-to-back compositing, early
 // termination) with the frame kernel's reconstruction and shading.
+// One short ray by one thread: the reference's _volume_ray loop
+// (R/render.py:380-453) over the ray's complete leaf list — exact restart chain,
+// lattice, sequential front-to-back compositing, early termination — with the
+// frame kernel's reconstruction and shading.  Used by k_short and by k_warp's
+// short-ray phase.
+template <int GRAD, bool ISO, bool COUNT>
+__device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __restrict__ s_tf, int64_t slot,
+                                          unsigned long long& my_reg, unsigned long long& my_smp,
+                                          unsigned long long& my_bytes) {
+    const SceneView& S = A.S;
+    const SlotPix sp = slot_pixel(A, slot);
+    Ray r;
+    pixel_ray(A, sp.x, sp.y, r);
+    const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
+    double tmin = 0.0, tmax = kTFar;
+    clip_ray(A.M, r, tmin, tmax);
+    if (ISO) tmax = A.iso_tend[slot];
+    const int count = A.leaf_count[slot] & kLeafCountMask;
+    const int32_t* __restrict__ list = A.leaves + slot * (int64_t)A.leaf_cap;
+    double ar = 0.0, ag = 0.0, ab = 0.0, aa = 0.0;
+    int nreg = 0, nsmp = 0;
+    double t = tmin;
+    for (int li = 0; li < count && aa < A.M.early; li++) {
+        const int rid = list[li];
+        const RegionRec rr = S.rec[rid];
+        double r_in, r_out;
+        slab_h(rr.lo, rr.hi, r, r_in, r_out);
+        const double ci = r_in > t ? r_in : t, co = r_out < tmax ? r_out : tmax;
+        if (!(ci < co)) continue;  // not the reference's next hit
+        nreg++;
+        const int lev = rr.meta >> 24, nids = rr.meta & 0xffffff;
+        const int32_t* ids = S.rids + rr.ids_begin;
+        if (COUNT) my_bytes += 32 + 4 * (unsigned long long)nids;
+        const double dt = A.M.lv_dt[lev];
+        double prev = ci, k = floor(ci / dt - rho) + 1.0;
+        bool done = false;
+        while (!done) {
+            double tk = dt * (k + rho);
+            k += 1.0;
+            if (tk >= co) { tk = co; done = true; }
+            else if (tk <= prev) continue;
+            const double sl = tk - prev, mid = 0.5 * (prev + tk);
+            prev = tk;
+            nsmp++;
+            const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1], pz = r.o[2] + mid * r.d[2];
+            FastAccum F;
+            gather_shade<GRAD == 1>(S, (int64_t)rr.ids_begin, nids, px, py, pz, F);
+            if (COUNT) my_bytes += 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
+            if (F.den > kEpsWeight) {
+                const double v = F.num / F.den;
+                double c[4];
+                tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_inv, v, c);
+                if (c[3] > 0.0) {
+                    const double alpha = opacity_correct(c[3], sl * A.M.lv_is1[lev]);
+                    if (GRAD != 0) {
+                        double f;
+                        if (GRAD == 1) {
+                            f = shade_factor_f(F.g, r);
+                        } else {
+                            double g[3];
+                            int64_t ne = 0;
+                            central_gradient(S, A.M.grad_mode, px, py, pz, rid, ids, nids, v, g, &ne);
+                            f = shade_factor(g, r);
+                        }
+                        c[0] *= f; c[1] *= f; c[2] *= f;
+                    }
+                    const double w = alpha * (1.0 - aa);
+                    ar += w * c[0];
+                    ag += w * c[1];
+                    ab += w * c[2];
+                    aa += w;
+                    if (aa >= A.M.early) break;
+                }
+            }
+        }
+        t = restart_t(co);
+        if (t >= tmax) break;
+    }
+    double acc[4] = {ar, ag, ab, aa};
+    if (ISO) {
+        const double f = A.iso_shade[slot];
+        if (f >= 0.0) {
+            const double wgt = 1.0 - acc[3];
+            acc[0] += wgt * A.M.iso_rgb[0] * f;
+            acc[1] += wgt * A.M.iso_rgb[1] * f;
+            acc[2] += wgt * A.M.iso_rgb[2] * f;
+            acc[3] = 1.0;
+        }
+    }
+    write_pixel(A, sp.out, acc, nreg, nsmp);
+    my_reg += nreg;
+    my_smp += nsmp;
+}
+
 template <int GRAD, bool ISO, bool COUNT>
 __global__ void __launch_bounds__(kWalkThreads) k_short(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     __shared__ double s_tf[1024];
@@ -994,92 +1088,7 @@ __global__ void __launch_bounds__(kWalkThreads) k_short(const __grid_constant__ 
     __syncthreads();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     unsigned long long my_reg = 0, my_smp = 0, my_bytes = 0;
-    if (i < n_short) {
-        const SceneView& S = A.S;
-        const int64_t slot = A.short_list[i];
-        const SlotPix sp = slot_pixel(A, slot);
-        Ray r;
-        pixel_ray(A, sp.x, sp.y, r);
-        const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
-        double tmin = 0.0, tmax = kTFar;
-        clip_ray(A.M, r, tmin, tmax);
-        if (ISO) tmax = A.iso_tend[slot];
-        const int count = A.leaf_count[slot] & kLeafCountMask;
-        const int32_t* __restrict__ list = A.leaves + slot * (int64_t)A.leaf_cap;
-        double ar = 0.0, ag = 0.0, ab = 0.0, aa = 0.0;
-        int nreg = 0, nsmp = 0;
-        double t = tmin;
-        for (int li = 0; li < count && aa < A.M.early; li++) {
-            const int rid = list[li];
-            const RegionRec rr = S.rec[rid];
-            double r_in, r_out;
-            slab_h(rr.lo, rr.hi, r, r_in, r_out);
-            const double ci = r_in > t ? r_in : t, co = r_out < tmax ? r_out : tmax;
-            if (!(ci < co)) continue;  // not the reference's next hit
-            nreg++;
-            const int lev = rr.meta >> 24, nids = rr.meta & 0xffffff;
-            const int32_t* ids = S.rids + rr.ids_begin;
-            if (COUNT) my_bytes += 32 + 4 * (unsigned long long)nids;
-            const double dt = A.M.lv_dt[lev];
-            double prev = ci, k = floor(ci / dt - rho) + 1.0;
-            bool done = false;
-            while (!done) {
-                double tk = dt * (k + rho);
-                k += 1.0;
-                if (tk >= co) { tk = co; done = true; }
-                else if (tk <= prev) continue;
-                const double sl = tk - prev, mid = 0.5 * (prev + tk);
-                prev = tk;
-                nsmp++;
-                const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1], pz = r.o[2] + mid * r.d[2];
-                FastAccum F;
-                gather_shade<GRAD == 1>(S, (int64_t)rr.ids_begin, nids, px, py, pz, F);
-                if (COUNT) my_bytes += 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
-                if (F.den > kEpsWeight) {
-                    const double v = F.num / F.den;
-                    double c[4];
-                    tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_inv, v, c);
-                    if (c[3] > 0.0) {
-                        const double alpha = opacity_correct(c[3], sl * A.M.lv_is1[lev]);
-                        if (GRAD != 0) {
-                            double f;
-                            if (GRAD == 1) {
-                                f = shade_factor_f(F.g, r);
-                            } else {
-                                double g[3];
-                                int64_t ne = 0;
-                                central_gradient(S, A.M.grad_mode, px, py, pz, rid, ids, nids, v, g, &ne);
-                                f = shade_factor(g, r);
-                            }
-                            c[0] *= f; c[1] *= f; c[2] *= f;
-                        }
-                        const double w = alpha * (1.0 - aa);
-                        ar += w * c[0];
-                        ag += w * c[1];
-                        ab += w * c[2];
-                        aa += w;
-                        if (aa >= A.M.early) break;
-                    }
-                }
-            }
-            t = restart_t(co);
-            if (t >= tmax) break;
-        }
-        double acc[4] = {ar, ag, ab, aa};
-        if (ISO) {
-            const double f = A.iso_shade[slot];
-            if (f >= 0.0) {
-                const double wgt = 1.0 - acc[3];
-                acc[0] += wgt * A.M.iso_rgb[0] * f;
-                acc[1] += wgt * A.M.iso_rgb[1] * f;
-                acc[2] += wgt * A.M.iso_rgb[2] * f;
-                acc[3] = 1.0;
-            }
-        }
-        write_pixel(A, sp.out, acc, nreg, nsmp);
-        my_reg = nreg;
-        my_smp = nsmp;
-    }
+    if (i < n_short) short_ray<GRAD, ISO, COUNT>(A, s_tf, (int64_t)A.short_list[i], my_reg, my_smp, my_bytes);
     for (int o = 16; o > 0; o >>= 1) {
         my_reg += __shfl_xor_sync(0xffffffffu, my_reg, o);
         my_smp += __shfl_xor_sync(0xffffffffu, my_smp, o);
@@ -1664,8 +1673,23 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             }
         }
     }
-    if (COUNT) {
-        for (int o = 16; o > 0; o >>= 1) tot_bytes += __shfl_xor_sync(FULL, tot_bytes, o);
+    // ---- short-ray phase (k_short fused): one short ray per lane, 32 per grab;
+    //      cheap, uniform rays fill the tail of the long-ray phase
+    if (A.fuse_short && A.leaves && !merged) {
+        const int64_t n_sh = (int64_t)A.walk_counter[0];
+        for (;;) {
+            unsigned long long c0 = 0;
+            if (lane == 0) c0 = atomicAdd(A.short_counter, 32ull);
+            c0 = __shfl_sync(FULL, c0, 0);
+            if ((int64_t)c0 >= n_sh) break;
+            const int64_t i = (int64_t)c0 + lane;
+            if (i < n_sh) short_ray<GRAD, ISO, COUNT>(A, s_tf, (int64_t)A.short_list[i], tot_reg, tot_smp, tot_bytes);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        tot_reg += __shfl_xor_sync(FULL, tot_reg, o);
+        tot_smp += __shfl_xor_sync(FULL, tot_smp, o);
+        if (COUNT) tot_bytes += __shfl_xor_sync(FULL, tot_bytes, o);
     }
     if (lane == 0 && A.stats) {
         atomicAdd(&A.stats[0], tot_reg);
@@ -1873,7 +1897,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             if (A.cut_list && A.walk_cap1 < A.leaf_cap)  // pass 2 over the cap-cut walks
                 XB_CUDA(cudaLaunchKernel((const void*)k_walk2, dim3(grid_for(n_slots, kWalkThreads)),
                                          dim3(kWalkThreads), wargs, 0, s));
-            if (A.short_list) {  // short rays -> k_short (when >= short_min of them), long ones -> k_warp
+            if (A.short_list && !A.fuse_short) {  // short rays -> k_short (when >= short_min of them)
                 using ShortFn = void (*)(RenderArgs, int64_t);
                 ShortFn sf;
                 if (g == 0) sf = iso ? (ShortFn)k_short<0, true, false> : (ShortFn)k_short<0, false, false>;

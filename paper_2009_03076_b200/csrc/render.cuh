@@ -50,6 +50,8 @@ struct RenderArgs {
     int32_t* long_list;                // rays for k_warp / k_iso_warp (k_route, in hit-list order)
     int32_t* any_list;                 // long + short rays, merged (k_warp's work when k_short is off)
     unsigned long long* dbg;           // diagnostics (XB_DEBUG_CHUNKS): k_warp chunks, chunk lanes, rays, samples
+    int fuse_short;                    // k_warp runs the short rays after the long ones (no k_short launch)
+    unsigned long long* short_counter; // k_warp's short-ray grab counter
     int cut_tau;                       // k_walk2 also continues walks stopped by the opacity minorant
     int32_t* blk_counts;               // k_walk -> k_route: short / long / cut rays per k_walk block
     int32_t* short_list;               // rays with a complete list of <= 8 leaves (k_short's work), or NULL

@@ -1,4 +1,2 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 900 python -m pytest tests/ -m gpu -x -q 2>&1 | tail -3
-python tools/e2e_probe.py c3 30 2>&1 | tail -8
-XB_BANDS=0 python tools/e2e_probe.py c3 30 2>&1 | grep -E "render_frame|pinned"
+for c in c3 c2 c5; do echo $c; python tools/ab.py $c "warp,e:XB_FUSE_SHORT=0" 2>&1 | tail -2 | cut -c1-70; XB_LIB=alt/libexabricks_head.so python tools/ab.py $c "warp" 2>&1 | tail -1 | cut -c1-70; python tools/ab.py $c "warp" 2>&1 | tail -1 | cut -c1-70; done
