@@ -200,7 +200,23 @@ def pixel_rho(pixel: int, seed: int) -> float:
 # native argument blocks
 
 
+_CAM_CACHE: dict = {}
+
+
 def camera_struct(camera: Camera) -> N.XbCamera:
+    """XbCamera of `camera`; cached on its fields (the numpy basis costs 30-70 us
+    per frame, more than the host side of the rest of the call)."""
+    key = (camera.position.tobytes(), camera.forward.tobytes(), camera.up.tobytes(), float(camera.fov_y),
+           int(camera.width), int(camera.height))
+    c = _CAM_CACHE.get(key)
+    if c is None:
+        if len(_CAM_CACHE) > 256:
+            _CAM_CACHE.clear()
+        c = _CAM_CACHE[key] = _camera_struct(camera)
+    return c
+
+
+def _camera_struct(camera: Camera) -> N.XbCamera:
     r, u, f = camera.basis()
     c = N.XbCamera()
     c.width, c.height = int(camera.width), int(camera.height)
