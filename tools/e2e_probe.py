@@ -47,6 +47,17 @@ def timeit(name, fn):
 timeit("python structs", lambda: (R.camera_struct(cam), R.march_struct(tf, params)))
 timeit("_host_image", lambda: R._host_image(H, W))
 timeit("D2H 4WH pinned", lambda: (pinned.copy_(dev), torch.cuda.synchronize()))
+def enqueue_only():
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    R.render_native(scene, cam, tf, params, dev.data_ptr(), sync=False)
+    dt = time.perf_counter() - t
+    torch.cuda.synchronize()
+    return dt
+
+
+enq = [enqueue_only() for _ in range(reps)]
+print(f"{'host enqueue (xb_render, no sync)':34s} median {np.median(enq) * 1e3:7.3f} ms", flush=True)
 timeit("render device out, no stats", lambda: (R.render_native(scene, cam, tf, params, dev.data_ptr(), sync=False),
                                                torch.cuda.synchronize()))
 timeit("render device out + stats", lambda: R.render_native(scene, cam, tf, params, dev.data_ptr()))
