@@ -503,16 +503,16 @@ def run_config(args, cfg, cfg_name, with_extras):
             "kernel_ms": ms_kernel, "wall_s_timed": wall,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "frame = k_classify + hit select + k_walk + k_route + k_walk2 + k_short + k_warp "
+                         "kernel": "frame = k_classify + hit select + k_walk + k_route + k_walk2 + k_warp (long, then short rays) "
                                    "(+ the iso phase) (csrc/render.cu); k_warp dominates; achieved over the whole "
                                    "frame's event time",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback 6.65 TB/s"},
             # our kernels per frame: k_classify, k_walk, k_warp (+ k_iso_pass) (+ k_unpack_tiles on rank 0
             # when tiled); the CUB select between k_classify and k_walk is library code
-            # own kernels per frame: k_classify, k_walk, k_route, k_walk2, k_short, k_warp (the CUB hit
-            # select adds two library kernels); the iso phase adds k_classify, k_walk, k_route, k_iso_warp;
-            # rank 0 of a tiled run adds k_unpack_tiles
-            "gpu_launches": args.steps * (6 + 4 * (cfg.get("iso") is not None) + (world > 1 and rank == 0)),
+            # own kernels per frame: k_classify, k_walk, k_route, k_walk2, k_warp (short rays included;
+            # the CUB hit select adds two library kernels); the iso phase adds k_classify, k_walk,
+            # k_route, k_iso_warp; rank 0 of a tiled run adds k_unpack_tiles
+            "gpu_launches": args.steps * (5 + 4 * (cfg.get("iso") is not None) + (world > 1 and rank == 0)),
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
