@@ -250,13 +250,15 @@ KERNEL_ENVS = {
     "warp": {},                        # default: k_classify + k_walk leaf lists + k_warp
     "warp_cap1": {"XB_LEAF_CAP": "1"},  # every long ray falls back to the warp frontier
     "warp_nowalk": {"XB_WALK": "0"},   # k_warp's frontier only
-    "warp_short": {"XB_SHORT": "1"},   # short rays through k_short (one thread per ray)
+    "warp_short": {"XB_SHORT": "1"},   # short rays one per lane (k_warp's second phase) even when few
+    "warp_kshort": {"XB_SHORT": "1", "XB_FUSE_SHORT": "0"},  # ... through the separate k_short launch
     "warp_2pass": {"XB_WALK_CAP1": "2", "XB_WALK2_MIN": "0"},  # k_walk2 continues (nearly) every walk
     "frame": {"XB_KERNEL": "frame"},   # per-lane persistent kernel
     "tile": {"XB_KERNEL": "tile"},     # one thread per pixel
     "lbvh": {"XB_TRAVERSAL": "lbvh"},  # per-visit LBVH closest-hit queries (the reference's traversal)
 }
-_ENV_KEYS = ("XB_KERNEL", "XB_LEAF_CAP", "XB_WALK", "XB_TRAVERSAL", "XB_SHORT", "XB_WALK_CAP1", "XB_WALK2_MIN")
+_ENV_KEYS = ("XB_KERNEL", "XB_LEAF_CAP", "XB_WALK", "XB_TRAVERSAL", "XB_SHORT", "XB_WALK_CAP1", "XB_WALK2_MIN",
+             "XB_FUSE_SHORT")
 
 
 @pytest.fixture
@@ -472,7 +474,7 @@ def test_acceptance_million_cells_vs_oracle(xb):
     # repetition
     import os
 
-    for kern in ("tile", "frame", "warp_cap1", "warp_nowalk", "warp_short", "warp_2pass", "lbvh"):
+    for kern in ("tile", "frame", "warp_cap1", "warp_nowalk", "warp_short", "warp_kshort", "warp_2pass", "lbvh"):
         os.environ.update(KERNEL_ENVS[kern])
         try:
             u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)
