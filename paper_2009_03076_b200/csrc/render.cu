@@ -371,6 +371,12 @@ constexpr int kRaysPerGrab = 8;  // rays taken per work-counter atomic
 // (first pipeline), C3 1.21 vs 0.92 and C2 8.74 vs 6.31 (walk lists).  Kept
 // for A/B.
 constexpr bool kFlatGather = false;
+// k_warp work statistics (XB_DEBUG_CHUNKS at run time; compiled in only with
+// `make DEBUG_CHUNKS=1`: the counters cost k_warp registers)
+#ifndef XB_DEBUG_CHUNKS
+#define XB_DEBUG_CHUNKS 0
+#endif
+constexpr bool kDebugChunks = XB_DEBUG_CHUNKS != 0;
 
 struct SegQ {       // one visited region of the segment queue
     double ci, co;   // clipped interval
@@ -1251,7 +1257,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                     if (pending >= 32 || (!walk && pending > 0)) {
                         // ================= one chunk of (up to) 32 samples
                         const int m = min(32, pending);
-                        if (A.dbg && lane == 0) {
+                        if (kDebugChunks && A.dbg && lane == 0) {
                             atomicAdd(A.dbg, 1ull);
                             atomicAdd(A.dbg + 1, (unsigned long long)m);
                         }
@@ -1282,7 +1288,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             py = r.o[1] + mid * r.d[1];
                             pz = r.o[2] + mid * r.d[2];
                         }
-                        if (A.dbg) {
+                        if (kDebugChunks && A.dbg) {
                             int nn = act ? nids : 0, mx = nn;
                             for (int o = 16; o > 0; o >>= 1) {
                                 nn += __shfl_xor_sync(FULL, nn, o);
@@ -1663,7 +1669,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                     }
                 }
                 write_pixel(A, out_px, acc, nreg, nsmp);
-                if (A.dbg) {
+                if (kDebugChunks && A.dbg) {
                     atomicAdd(A.dbg + 2, 1ull);
                     atomicAdd(A.dbg + 3, (unsigned long long)nsmp);
                     atomicAdd(A.dbg + 4, (unsigned long long)nreg);

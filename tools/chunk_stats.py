@@ -1,4 +1,5 @@
-"""k_warp work statistics (XB_DEBUG_CHUNKS): python tools/chunk_stats.py CONFIG"""
+"""k_warp work statistics (XB_DEBUG_CHUNKS; needs a library built with `make DEBUG_CHUNKS=1`):
+python tools/chunk_stats.py CONFIG"""
 import os
 import sys
 
