@@ -644,9 +644,6 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->short_leaves = 8;
         A->short_samples = 24.f;
         A->leaf_cap = 0;
-        A->cap_div = 0;
-        A->cap_min = 1;
-        A->walk_budget = 0;
         {
             const char* ek = getenv("XB_KERNEL");
             const char* ew = getenv("XB_WALK");
@@ -654,21 +651,18 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             if (walk) {
                 keep_pool(m->m.device);
                 const char* ec = getenv("XB_LEAF_CAP");
-                // Leaf cap per walk (then k_warp resumes the rest).  Sweep with resume, ms/frame:
+                // Leaf cap per walk (then k_warp resumes the rest).  Single-pass sweep with resume,
+                // ms/frame (first pipeline):
                 //   cap      16    32    48    64    96    128
                 //   C2     7.54  7.08  6.81  6.62  6.42  6.47     (357K candidate rays, ~46 visits each)
                 //   C3     1.48  1.52  1.57  1.61  1.76  1.98     (312K candidates, ~6 visits, long tail)
                 //   C5                 3.37        3.40           (272K candidates)
                 // C3's few very long walks set k_walk's length; C2's many long walks are cheaper in
                 // k_walk than in the frontier.  Neither the candidate count (similar in all three) nor a
-                // clock budget (tools/ab.py: budgets cost C2 15-25 %) separates them, so: a fixed 64.
+                // clock budget per walk (C2 +15-25 %) separates them: hence the two passes below
+                // (16 leaves, then k_walk2 to 96 when many walks were cut).
                 const char* ec2 = getenv("XB_WALK_CAP2");
                 const int cap = ec ? std::max(1, atoi(ec)) : (ec2 ? std::max(1, atoi(ec2)) : 96);
-                const char* ed = getenv("XB_CAP_DIV");
-                A->cap_div = ed ? atoi(ed) : 0;
-                A->cap_min = 16;
-                const char* eb = getenv("XB_WALK_BUDGET");
-                A->walk_budget = eb ? atoll(eb) : 0;
                 const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
                 const size_t ns1 = std::max<size_t>(n_slots, 1);
                 const size_t res_words = 1 + 3 * 48;  // render.cu kResume

@@ -558,13 +558,11 @@ __device__ __forceinline__ void walk_leaves(const RenderArgs& A, int64_t slot, c
                                             float* st_tn, float* st_tf, int sp_n, int32_t* __restrict__ out,
                                             int& count, int& flags, int cap, float& est) {
     const SceneView& S = A.S;
-    const long long budget = A.walk_budget;
     const float spc = (float)A.M.spc, tau_stop = A.walk_tau_stop;
     float tau = 0.f;
-    const long long t_begin = clock64();
     for (;;) {
         if (code <= -2) {  // a leaf: list it
-            if (count == cap || (budget > 0 && clock64() - t_begin > budget)) {  // resume from this leaf
+            if (count == cap) {  // resume from this leaf
                 flags = kLeafTruncated;
                 save_resume(A, slot, code, tn, tf, st_code, st_tn, st_tf, sp_n);
                 break;

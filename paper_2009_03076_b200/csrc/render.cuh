@@ -41,8 +41,6 @@ struct RenderArgs {
     int walk_cap1;                     // k_walk's cap (pass 1)
     long long walk2_min;               // k_walk2 runs only for at least this many cap-cut walks
     int32_t* cut_list;                 // walks cut at walk_cap1 (k_walk2's work)
-    int cap_div, cap_min;              // k_walk's effective cap = clamp(n_candidates / cap_div, cap_min, leaf_cap)
-    long long walk_budget;             // k_walk: clock cycles per walk before it hands over (0 = none)
     int32_t* resume;                   // per slot: k_walk's ordered remainder when truncated (1 + 3 x kResume words)
     const float* vqmin;                // per region opacity minorant (k_walk early stop), may be NULL
     unsigned long long* walk_counter;  // list lengths: [0] short, [1] long, [2] cut, [3] hit, [4] any

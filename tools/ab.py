@@ -33,7 +33,7 @@ def setv(v):
         os.environ.pop(k)
     """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N) | gD (guided grab divisor D)"""
     for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU",
-              "XB_TRAVERSAL", "XB_CAP_DIV", "XB_WALK_BUDGET", "XB_SHORT", "XB_SHORT_LEAVES", "XB_SHORT_SAMPLES"):
+              "XB_TRAVERSAL", "XB_SHORT", "XB_SHORT_LEAVES", "XB_SHORT_SAMPLES"):
         os.environ.pop(k, None)
     for k in ("XB_WALK_CAP1", "XB_WALK2_MIN", "XB_WALK_CAP2", "XB_CUT_TAU"):
         os.environ.pop(k, None)
@@ -58,10 +58,6 @@ def setv(v):
         os.environ["XB_SHORT"] = "1"
     elif v == "noshort":
         os.environ["XB_SHORT"] = "0"
-    elif v.startswith("bud") and v[3:].isdigit():
-        os.environ["XB_WALK_BUDGET"] = v[3:]
-    elif v.startswith("div") and v[3:].isdigit():
-        os.environ["XB_CAP_DIV"] = v[3:]
     elif v == "lbvh":
         os.environ["XB_TRAVERSAL"] = "lbvh"
     elif v == "notau":
