@@ -724,14 +724,18 @@ route:
 // before it, ranks its rays with ballots and writes them; the last block
 // publishes the list lengths.  (Order matters for speed, not results: lists in
 // walk-completion order cost C3 16 %, C2 8 % in k_warp / k_short locality.)
+constexpr int kRouteSub = 4;  // k_walk blocks (128 hits each) per k_route block
+
 __global__ void __launch_bounds__(kWalkThreads) k_route(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     __shared__ int s_sum[3][kWalkThreads / 32];
+    __shared__ int s_w[3][kWalkThreads / 32];
     const int64_t n_cand = (int64_t)A.walk_counter[3];
-    const int64_t nb = (n_cand + blockDim.x - 1) / blockDim.x;
-    if ((int64_t)blockIdx.x >= nb) return;
+    const int64_t nb = (n_cand + kWalkThreads - 1) / kWalkThreads;
+    const int64_t bfirst = blockIdx.x * (int64_t)kRouteSub;
+    if (bfirst >= nb) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int p0 = 0, p1 = 0, p2 = 0;  // route counts of the blocks before this one
-    for (int64_t j = threadIdx.x; j < (int64_t)blockIdx.x; j += blockDim.x) {
+    int p0 = 0, p1 = 0, p2 = 0;  // route counts of the k_walk blocks before this one's first
+    for (int64_t j = threadIdx.x; j < bfirst; j += blockDim.x) {
         p0 += A.blk_counts[3 * j];
         p1 += A.blk_counts[3 * j + 1];
         p2 += A.blk_counts[3 * j + 2];
@@ -741,40 +745,47 @@ __global__ void __launch_bounds__(kWalkThreads) k_route(const __grid_constant__ 
         p1 += __shfl_xor_sync(0xffffffffu, p1, o);
         p2 += __shfl_xor_sync(0xffffffffu, p2, o);
     }
-    const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    bool is_short = false, is_long = false, is_cut = false;
-    int64_t slot = 0;
-    if (ci < n_cand) {
-        slot = A.hit_list[ci];
-        route_of(A, A.leaf_count[slot], is_short, is_long, is_cut);
-    }
-    const unsigned lt = (1u << lane) - 1u;
-    const unsigned ms = __ballot_sync(0xffffffffu, is_short), ml = __ballot_sync(0xffffffffu, is_long),
-                   mc = __ballot_sync(0xffffffffu, is_cut);
-    __shared__ int s_w[3][kWalkThreads / 32];
-    if (lane == 0) {
-        s_sum[0][wid] = p0; s_sum[1][wid] = p1; s_sum[2][wid] = p2;
-        s_w[0][wid] = __popc(ms); s_w[1][wid] = __popc(ml); s_w[2][wid] = __popc(mc);
-    }
+    if (lane == 0) { s_sum[0][wid] = p0; s_sum[1][wid] = p1; s_sum[2][wid] = p2; }
     __syncthreads();
-    int b0 = 0, b1 = 0, b2 = 0, w0 = 0, w1 = 0, w2 = 0;
+    int b0 = 0, b1 = 0, b2 = 0;  // list offsets of the current 128 hits
 #pragma unroll
-    for (int w = 0; w < kWalkThreads / 32; w++) {
-        b0 += s_sum[0][w]; b1 += s_sum[1][w]; b2 += s_sum[2][w];
-        if (w < wid) { w0 += s_w[0][w]; w1 += s_w[1][w]; w2 += s_w[2][w]; }
-    }
-    if (is_short) A.short_list[b0 + w0 + __popc(ms & lt)] = (int32_t)slot;
-    if (is_long) A.long_list[b1 + w1 + __popc(ml & lt)] = (int32_t)slot;
-    if (is_cut) A.cut_list[b2 + w2 + __popc(mc & lt)] = (int32_t)slot;
-    if (A.any_list && (is_short || is_long))  // short + long merged, in hit order
-        A.any_list[b0 + b1 + w0 + w1 + __popc((ms | ml) & lt)] = (int32_t)slot;
-    if ((int64_t)blockIdx.x == nb - 1 && threadIdx.x == 0) {
-        int t0 = b0, t1 = b1, t2 = b2;
-        for (int w = 0; w < kWalkThreads / 32; w++) { t0 += s_w[0][w]; t1 += s_w[1][w]; t2 += s_w[2][w]; }
-        A.walk_counter[0] = (unsigned long long)t0;
-        A.walk_counter[1] = (unsigned long long)t1;
-        A.walk_counter[2] = (unsigned long long)t2;
-        A.walk_counter[4] = (unsigned long long)(t0 + t1);
+    for (int w = 0; w < kWalkThreads / 32; w++) { b0 += s_sum[0][w]; b1 += s_sum[1][w]; b2 += s_sum[2][w]; }
+    const unsigned lt = (1u << lane) - 1u;
+    for (int sub = 0; sub < kRouteSub; sub++) {
+        const int64_t bb = bfirst + sub;
+        if (bb >= nb) break;  // uniform over the block
+        const int64_t ci = bb * kWalkThreads + threadIdx.x;
+        bool is_short = false, is_long = false, is_cut = false;
+        int64_t slot = 0;
+        if (ci < n_cand) {
+            slot = A.hit_list[ci];
+            route_of(A, A.leaf_count[slot], is_short, is_long, is_cut);
+        }
+        const unsigned ms = __ballot_sync(0xffffffffu, is_short), ml = __ballot_sync(0xffffffffu, is_long),
+                       mc = __ballot_sync(0xffffffffu, is_cut);
+        __syncthreads();  // the previous round's s_w reads are done
+        if (lane == 0) { s_w[0][wid] = __popc(ms); s_w[1][wid] = __popc(ml); s_w[2][wid] = __popc(mc); }
+        __syncthreads();
+        int w0 = 0, w1 = 0, w2 = 0, t0 = 0, t1 = 0, t2 = 0;
+#pragma unroll
+        for (int w = 0; w < kWalkThreads / 32; w++) {
+            if (w < wid) { w0 += s_w[0][w]; w1 += s_w[1][w]; w2 += s_w[2][w]; }
+            t0 += s_w[0][w]; t1 += s_w[1][w]; t2 += s_w[2][w];
+        }
+        if (is_short) A.short_list[b0 + w0 + __popc(ms & lt)] = (int32_t)slot;
+        if (is_long) A.long_list[b1 + w1 + __popc(ml & lt)] = (int32_t)slot;
+        if (is_cut) A.cut_list[b2 + w2 + __popc(mc & lt)] = (int32_t)slot;
+        if (A.any_list && (is_short || is_long))  // short + long merged, in hit order
+            A.any_list[b0 + b1 + w0 + w1 + __popc((ms | ml) & lt)] = (int32_t)slot;
+        b0 += t0;
+        b1 += t1;
+        b2 += t2;
+        if (bb == nb - 1 && threadIdx.x == 0) {  // the last 128 hits: the list lengths
+            A.walk_counter[0] = (unsigned long long)b0;
+            A.walk_counter[1] = (unsigned long long)b1;
+            A.walk_counter[2] = (unsigned long long)b2;
+            A.walk_counter[4] = (unsigned long long)(b0 + b1);
+        }
     }
     (void)n_slots;
 }
@@ -1836,8 +1847,8 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         hit_select(*Ai, n_slots, s);
         XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads), iargs,
                                  0, s));
-        XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
-                                 iargs, 0, s));
+        XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads * kRouteSub)),
+                                 dim3(kWalkThreads), iargs, 0, s));
         if (getenv("XB_ISO_LANE")) {  // A/B: one thread per iso ray
             const void* mf = count ? (const void*)k_iso_march<true> : (const void*)k_iso_march<false>;
             XB_CUDA(cudaLaunchKernel(mf, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads), iargs, 0, s));
@@ -1901,8 +1912,8 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             // k_route builds the short / long / cut lists
             XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
                                      wargs, 0, s));
-            XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
-                                     wargs, 0, s));
+            XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads * kRouteSub)),
+                                     dim3(kWalkThreads), wargs, 0, s));
             if (A.cut_list && A.walk_cap1 < A.leaf_cap)  // pass 2 over the cap-cut walks
                 XB_CUDA(cudaLaunchKernel((const void*)k_walk2, dim3(grid_for(n_slots, kWalkThreads)),
                                          dim3(kWalkThreads), wargs, 0, s));
