@@ -150,6 +150,27 @@ typedef struct {
 int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* vol, const xb_active* iso,
               const xb_camera* cam, const xb_march* mp, int32_t tile_rank, int32_t tile_world, void* rgba8,
               double* rgba_f64, int32_t* px_counts, int64_t* stats, int32_t count_bytes, void* stream);
+/* ---- frame-pipeline variants: A/B measurement and the parity matrix ----
+ * Process-wide; xb_render / xb_integrate_rays take a snapshot when called.
+ * The compiled defaults (xb_tuning_defaults) are the measured best
+ * (DESIGN.md §5); nothing else — no environment variable — changes the
+ * production path. */
+typedef struct {
+    int32_t kernel;     /* 0 (default): k_classify -> walk -> k_warp pipeline; 1: one thread per pixel (k_render) */
+    int32_t traversal;  /* 0 (default): ordered k-d walk; 1: per-visit LBVH closest-hit queries, the
+                           reference's traversal (R/accel.py:285-352; runs in the one-thread-per-pixel kernel) */
+    int32_t walk_lists; /* 1 (default): k_walk leaf lists; 0: k_warp's warp frontier from the root only */
+    int32_t leaf_cap;   /* 0 (default): two-pass walk (walk_cap1, then k_walk2 to 96); N > 0: one pass of N */
+    int32_t walk_cap1;  /* pass-1 leaf cap of the two-pass walk (default 16; clamped to the list capacity) */
+    int32_t short_rays; /* -1 (default): lane-per-ray phase when >= 1000 x SMs short rays; 0: never; 1: always */
+    int64_t walk2_min;  /* k_walk2 runs when >= walk2_min walks were cut; -1 (default): 500 x SMs */
+    int32_t fuse_short; /* 1 (default): short rays run inside k_warp after the long ones; 0: separate k_short */
+    int32_t reserved;
+} xb_tuning;
+void xb_tuning_defaults(xb_tuning* t);
+int xb_tuning_get(xb_tuning* t);
+int xb_tuning_set(const xb_tuning* t); /* NULL restores the defaults */
+
 int xb_tile_count(int32_t width, int32_t height, int32_t rank, int32_t world, int64_t* n_tiles, int32_t* tile_px);
 /* gathered packed tiles (rank-major, tiles_per_rank each) -> (H, W, 4) image; device pointers */
 int xb_unpack_tiles(const void* packed, int64_t tiles_per_rank, int32_t world, int32_t width, int32_t height,

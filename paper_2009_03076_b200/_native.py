@@ -53,6 +53,13 @@ class XbSynthSpec(C.Structure):
                 ("n_waves", i32), ("waves", (f64 * 5) * 8)]
 
 
+class XbTuning(C.Structure):
+    """xb_tuning (include/exabricks.h): frame-pipeline variants for A/B runs and the parity matrix."""
+
+    _fields_ = [("kernel", i32), ("traversal", i32), ("walk_lists", i32), ("leaf_cap", i32), ("walk_cap1", i32),
+                ("short_rays", i32), ("walk2_min", i64), ("fuse_short", i32), ("reserved", i32)]
+
+
 # exported symbol -> (restype, argtypes); tests check every declared symbol
 SIGNATURES = {
     "xb_last_error": (C.c_char_p, []),
@@ -83,6 +90,9 @@ SIGNATURES = {
     "xb_active_prims": (C.c_int, [P, P]),
     "xb_active_free": (None, [P]),
     "xb_render": (C.c_int, [P, P, i32, P, P, P, P, i32, i32, P, P, P, P, i32, P]),
+    "xb_tuning_defaults": (None, [P]),
+    "xb_tuning_get": (C.c_int, [P]),
+    "xb_tuning_set": (C.c_int, [P]),
     "xb_tile_count": (C.c_int, [i32, i32, i32, i32, P, P]),
     "xb_unpack_tiles": (C.c_int, [P, i64, i32, i32, i32, P, P]),
     "xb_integrate_rays": (C.c_int, [P, P, i32, P, P, i64, P, P, P, P, P, P, P]),
@@ -127,6 +137,31 @@ def check(rc):
     if rc != XB_OK:
         msg = lib().xb_last_error()
         raise NativeError(rc, msg.decode() if msg else "")
+
+
+class tuning:
+    """Context manager selecting frame-pipeline variants (xb_tuning_set), e.g.
+    `with tuning(kernel=1): ...`; restores the previous setting on exit.  The
+    setting is process-wide: the library's defaults are the production path."""
+
+    def __init__(self, **fields):
+        self.fields = fields
+        self.prev = None
+
+    def __enter__(self):
+        self.prev = XbTuning()
+        check(lib().xb_tuning_get(C.byref(self.prev)))
+        t = XbTuning()
+        lib().xb_tuning_defaults(C.byref(t))
+        for k, v in self.fields.items():
+            if not hasattr(t, k):
+                raise ValueError(f"unknown tuning field {k!r}")
+            setattr(t, k, int(v))
+        check(lib().xb_tuning_set(C.byref(t)))
+        return t
+
+    def __exit__(self, *exc):
+        check(lib().xb_tuning_set(C.byref(self.prev)))
 
 
 _dev_ok = {}

@@ -30,8 +30,7 @@ struct xb_regions {
     int64_t model_bricks = 0;
     // brick records in region-list order for the frame gather (built on first render)
     mutable std::mutex rb_mu;
-    mutable xb::DevBuf<int4> rb_a;
-    mutable xb::DevBuf<uint32_t> rb_m;
+    mutable xb::DevBuf<xb::RbRec> rb;
     mutable bool rb_ok = false;
 };
 struct xb_active {
@@ -92,25 +91,31 @@ void keep_pool(int device) {
     done[device] = true;
 }
 
+// frame-gather brick records in region-list order (march.cuh:RbRec)
 __global__ void k_region_bricks(const int32_t* __restrict__ ids, int64_t n, const int4* __restrict__ ba,
-                                const uint32_t* __restrict__ bm, int4* __restrict__ ra, uint32_t* __restrict__ rm) {
+                                const uint32_t* __restrict__ bm, xb::RbRec* __restrict__ rb) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int b = ids[i];
-    ra[i] = ba[b];
-    rm[i] = bm[b];
+    const int4 a = ba[b];
+    xb::RbRec r;
+    r.lx = (double)a.x;
+    r.ly = (double)a.y;
+    r.lz = (double)a.z;
+    r.off = (uint32_t)a.w;
+    r.meta = bm[b];
+    rb[i] = r;
 }
 
 void ensure_region_bricks(const xb_model* m, const xb_regions* r) {
     std::lock_guard<std::mutex> g(r->rb_mu);
     if (r->rb_ok) return;
     const int64_t n = std::max<int64_t>(r->r.n_ids, 1);
-    r->rb_a.alloc(n);
-    r->rb_m.alloc(n);
+    r->rb.alloc(n);
     if (r->r.n_ids > 0) {
         OwnedStream st;
         k_region_bricks<<<(unsigned)((r->r.n_ids + 255) / 256), 256, 0, st.s>>>(
-            r->r.ids.p, r->r.n_ids, m->m.brick_a.p, m->m.brick_m.p, r->rb_a.p, r->rb_m.p);
+            r->r.ids.p, r->r.n_ids, m->m.brick_a.p, m->m.brick_m.p, r->rb.p);
         XB_CUDA(cudaGetLastError());
         XB_CUDA(cudaStreamSynchronize(st.s));
     }
@@ -130,8 +135,7 @@ xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     S.rec = r->r.rec.p;
     S.rids = r->r.ids.p;
     ensure_region_bricks(m, r);
-    S.rb_a = r->rb_a.p;
-    S.rb_m = r->rb_m.p;
+    S.rb = r->rb.p;
     S.kd = r->r.kd.p;
     S.kd4 = r->r.kd4.p;
     for (int a = 0; a < 3; a++) {
@@ -546,13 +550,63 @@ int xb_tile_count(int32_t width, int32_t height, int32_t rank, int32_t world, in
     });
 }
 
+namespace {
+std::mutex g_tuning_mu;
+xb_tuning g_tuning = [] {
+    xb_tuning t;
+    xb_tuning_defaults(&t);
+    return t;
+}();
+
+xb_tuning tuning_snapshot() {
+    std::lock_guard<std::mutex> g(g_tuning_mu);
+    return g_tuning;
+}
+}  // namespace
+
+void xb_tuning_defaults(xb_tuning* t) {
+    if (!t) return;
+    std::memset(t, 0, sizeof(*t));
+    t->kernel = 0;
+    t->traversal = 0;
+    t->walk_lists = 1;
+    t->leaf_cap = 0;
+    t->walk_cap1 = 16;
+    t->short_rays = -1;
+    t->walk2_min = -1;
+    t->fuse_short = 1;
+}
+
+int xb_tuning_get(xb_tuning* t) {
+    return guarded([&] {
+        XB_CHECK(t, XB_ERR_ARG, "null tuning");
+        *t = tuning_snapshot();
+    });
+}
+
+int xb_tuning_set(const xb_tuning* t) {
+    return guarded([&] {
+        xb_tuning n;
+        if (t) n = *t; else xb_tuning_defaults(&n);
+        XB_CHECK(n.kernel == 0 || n.kernel == 1, XB_ERR_ARG, "tuning.kernel must be 0 or 1");
+        XB_CHECK(n.traversal == 0 || n.traversal == 1, XB_ERR_ARG, "tuning.traversal must be 0 or 1");
+        XB_CHECK(n.leaf_cap >= 0 && n.leaf_cap <= 4096, XB_ERR_ARG, "tuning.leaf_cap out of range");
+        XB_CHECK(n.walk_cap1 >= 1, XB_ERR_ARG, "tuning.walk_cap1 must be >= 1");
+        XB_CHECK(n.short_rays >= -1 && n.short_rays <= 1, XB_ERR_ARG, "tuning.short_rays must be -1, 0 or 1");
+        std::lock_guard<std::mutex> g(g_tuning_mu);
+        g_tuning = n;
+    });
+}
+
 int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* vol, const xb_active* iso,
               const xb_camera* cam, const xb_march* mp, int32_t tile_rank, int32_t tile_world, void* rgba8,
               double* rgba_f64, int32_t* px_counts, int64_t* stats, int32_t count_bytes, void* stream) {
     return guarded([&] {
+        XB_CHECK(m && r && vol, XB_ERR_ARG, "null model, regions or volume active set");
         XB_CHECK(cam && mp && rgba8, XB_ERR_ARG, "null camera, params or output");
         XB_CHECK(cam->width >= 1 && cam->height >= 1, XB_ERR_ARG, "image must be at least 1x1 pixel");
         XB_CHECK(tile_world >= 1 && tile_rank >= 0 && tile_rank < tile_world, XB_ERR_ARG, "bad tile rank/world");
+        const xb_tuning T = tuning_snapshot();
         xb::DeviceGuard g(m->m.device);
         cudaStream_t s = (cudaStream_t)stream;
         xb::RenderArgs* A = new xb::RenderArgs();  // 8.6 KB: keep off the stack
@@ -563,15 +617,13 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->vmask4 = vol->a.mask4.p;
         XB_CHECK(!mp->use_tree || m->m.n_tree > 0, XB_ERR_NO_TREE,
                  "cell-location sampling requires a model with the split tree");
-        A->use_lbvh = 0;
-        {
-            const char* tr = getenv("XB_TRAVERSAL");
-            if (tr && strcmp(tr, "lbvh") == 0) {
-                A->use_lbvh = 1;
-                A->vlb = xb::active_lbvh(r->r, vol->a, s).view();
-                A->ilb = (mp->iso_on && iso) ? xb::active_lbvh(r->r, iso->a, s).view() : A->vlb;
-            }
+        A->use_lbvh = T.traversal == 1;
+        if (A->use_lbvh) {
+            A->vlb = xb::active_lbvh(r->r, vol->a, s).view();
+            A->ilb = (mp->iso_on && iso) ? xb::active_lbvh(r->r, iso->a, s).view() : A->vlb;
         }
+        // one thread per pixel for the LBVH traversal and the cell-location gather
+        A->kernel = (T.kernel == 1 || A->use_lbvh || mp->use_tree) ? 1 : 0;
         A->vqmin = vol->a.qmin.n ? vol->a.qmin.p : nullptr;
         A->wflags = A->vflags;
         A->wmask4 = A->vmask4;
@@ -619,9 +671,11 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         unsigned long long* dstats = (stats || count_bytes) ? scratch : nullptr;
         A->stats = dstats;
         A->work_counter = scratch + 3;
-        A->dbg = getenv("XB_DEBUG_CHUNKS") ? scratch + 9 : nullptr;  // [9, 16)
+        A->dbg = xb::kDebugChunks ? scratch + 9 : nullptr;  // [9, 16): make DEBUG_CHUNKS=1 builds only
         A->short_counter = scratch + 16;
-        A->fuse_short = getenv("XB_FUSE_SHORT") ? atoi(getenv("XB_FUSE_SHORT")) : 1;
+        A->fuse_short = T.fuse_short != 0;
+        A->grab_div = 4;
+        A->grab_fixed = 0;
         double* iso_buf = nullptr;
         if (A->M.iso_on) {
             const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
@@ -629,8 +683,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             A->iso_tend = iso_buf;
             A->iso_shade = iso_buf + n_slots;
         }
-        // k_walk -> k_warp leaf lists (the default warp kernel; XB_WALK=0 or another
-        // XB_KERNEL runs the frontier-only path)
+        // k_walk -> k_warp leaf lists (the default pipeline; tuning.walk_lists = 0 runs k_warp's
+        // frontier-only path)
         int32_t* leaf_buf = nullptr;
         A->leaves = nullptr;
         A->leaf_count = nullptr;
@@ -641,82 +695,53 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->walk_cap1 = 0;
         A->walk2_min = 0;
         A->cut_list = nullptr;
-        A->short_leaves = 8;
-        A->short_samples = 24.f;
+        A->short_leaves = xb::kShortLeaves;
+        A->short_samples = xb::kShortSamples;
         A->leaf_cap = 0;
-        {
-            const char* ek = getenv("XB_KERNEL");
-            const char* ew = getenv("XB_WALK");
-            const bool walk = !(ek && (strcmp(ek, "frame") == 0 || strcmp(ek, "tile") == 0)) && !(ew && ew[0] == '0');
-            if (walk) {
-                keep_pool(m->m.device);
-                const char* ec = getenv("XB_LEAF_CAP");
-                // Leaf cap per walk (then k_warp resumes the rest).  Single-pass sweep with resume,
-                // ms/frame (first pipeline):
-                //   cap      16    32    48    64    96    128
-                //   C2     7.54  7.08  6.81  6.62  6.42  6.47     (357K candidate rays, ~46 visits each)
-                //   C3     1.48  1.52  1.57  1.61  1.76  1.98     (312K candidates, ~6 visits, long tail)
-                //   C5                 3.37        3.40           (272K candidates)
-                // C3's few very long walks set k_walk's length; C2's many long walks are cheaper in
-                // k_walk than in the frontier.  Neither the candidate count (similar in all three) nor a
-                // clock budget per walk (C2 +15-25 %) separates them: hence the two passes below
-                // (16 leaves, then k_walk2 to 96 when many walks were cut).
-                const char* ec2 = getenv("XB_WALK_CAP2");
-                const int cap = ec ? std::max(1, atoi(ec)) : (ec2 ? std::max(1, atoi(ec2)) : 96);
-                const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
-                const size_t ns1 = std::max<size_t>(n_slots, 1);
-                const size_t res_words = 1 + 3 * 48;  // render.cu kResume
-                const size_t nblk = (ns1 + xb::kWalkThreads - 1) / xb::kWalkThreads;
-                XB_CUDA(cudaMallocAsync((void**)&leaf_buf, (ns1 * (cap + 6 + res_words) + 3 * nblk) * sizeof(int32_t), s));
-                A->leaf_count = leaf_buf;
-                A->hit_list = leaf_buf + ns1;
-                // two-pass walk: pass 1 caps at 16 leaves; pass 2 continues the cap-cut walks to the
-                // list capacity (96) when there are >= 500 x SMs of them.  tools/ab.py, ms (C3 / C2 /
-                // C5): single cap 64: 1.39 / 6.72 / 3.45; 24+96: 1.22 / 6.54 / 3.75; 16+96: 1.20 /
-                // 6.55 / 3.64; 16+64: 1.19 / 6.73 / 3.51.
-                const char* e1 = getenv("XB_WALK_CAP1");
-                A->walk_cap1 = ec ? cap : (e1 ? std::max(1, atoi(e1)) : 16);
-                const char* e2 = getenv("XB_WALK2_MIN");
-                A->cut_list = leaf_buf + (3 + res_words + cap) * ns1;
-                A->long_list = leaf_buf + (4 + res_words + cap) * ns1;
-                A->any_list = leaf_buf + (5 + res_words + cap) * ns1;
-                A->blk_counts = leaf_buf + (6 + res_words + cap) * ns1;
-                A->cut_tau = getenv("XB_CUT_TAU") ? atoi(getenv("XB_CUT_TAU")) : 1;
-                // k_short for rays with <= 8 leaves and <= 24 estimated samples, used only when the
-                // frame has >= 1000 x SMs of them (decided on the device).  tools/ab.py, ms, forced on
-                // vs off: C3 (270K short rays) 1.56 vs 1.61, C5 (44K) 3.70 vs 3.40, C2 (57K) 6.82 vs
-                // 6.66 — one thread per ray pays only when short rays are plentiful.  XB_SHORT=0 / 1:
-                // never / always.
-                const char* esh = getenv("XB_SHORT");
-                int sms = 148;
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->m.device);
-                A->short_list = (esh && esh[0] == '0') ? nullptr : leaf_buf + 2 * ns1;
-                A->short_min = (esh && esh[0] == '1') ? 0 : 1000ll * sms;
-                A->short_leaves = getenv("XB_SHORT_LEAVES") ? atoi(getenv("XB_SHORT_LEAVES")) : 8;
-                A->walk2_min = e2 ? atoll(e2) : 500ll * sms;
-                A->short_samples = getenv("XB_SHORT_SAMPLES") ? (float)atof(getenv("XB_SHORT_SAMPLES")) : 24.f;
-                A->resume = leaf_buf + 3 * ns1;
-                A->leaves = leaf_buf + (3 + res_words) * ns1;
-                A->leaf_cap = cap;
-            }
+        A->cut_tau = 1;
+        if (A->kernel == 0 && T.walk_lists) {
+            keep_pool(m->m.device);
+            // Leaf cap per walk (then k_warp resumes the rest).  Single-pass sweep with resume,
+            // ms/frame (round-1 pipeline):
+            //   cap      16    32    48    64    96    128
+            //   C2     7.54  7.08  6.81  6.62  6.42  6.47     (357K candidate rays, ~46 visits each)
+            //   C3     1.48  1.52  1.57  1.61  1.76  1.98     (312K candidates, ~6 visits, long tail)
+            //   C5                 3.37        3.40           (272K candidates)
+            // C3's few very long walks set k_walk's length; C2's many long walks are cheaper in
+            // k_walk than in the frontier.  Neither the candidate count (similar in all three) nor a
+            // clock budget per walk (C2 +15-25 %) separates them: hence the two passes below
+            // (16 leaves, then k_walk2 to 96 when many walks were cut).
+            const int cap = T.leaf_cap > 0 ? T.leaf_cap : 96;
+            const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;
+            const size_t ns1 = std::max<size_t>(n_slots, 1);
+            const size_t res_words = 1 + 3 * xb::kResume;
+            const size_t nblk = (ns1 + xb::kWalkThreads - 1) / xb::kWalkThreads;
+            XB_CUDA(cudaMallocAsync((void**)&leaf_buf, (ns1 * (cap + 6 + res_words) + 3 * nblk) * sizeof(int32_t), s));
+            A->leaf_count = leaf_buf;
+            A->hit_list = leaf_buf + ns1;
+            // two-pass walk: pass 1 caps at 16 leaves; pass 2 continues the cap-cut walks to the
+            // list capacity (96) when there are >= 500 x SMs of them.  tools/ab.py, ms (C3 / C2 /
+            // C5): single cap 64: 1.39 / 6.72 / 3.45; 24+96: 1.22 / 6.54 / 3.75; 16+96: 1.20 /
+            // 6.55 / 3.64; 16+64: 1.19 / 6.73 / 3.51.
+            A->walk_cap1 = T.leaf_cap > 0 ? cap : std::min(cap, std::max(1, T.walk_cap1));
+            A->cut_list = leaf_buf + (3 + res_words + cap) * ns1;
+            A->long_list = leaf_buf + (4 + res_words + cap) * ns1;
+            A->any_list = leaf_buf + (5 + res_words + cap) * ns1;
+            A->blk_counts = leaf_buf + (6 + res_words + cap) * ns1;
+            // short rays (<= 8 leaves, <= 24 estimated samples) run one per lane, used only when the
+            // frame has >= 1000 x SMs of them (decided on the device).  tools/ab.py, ms, forced on
+            // vs off: C3 (270K short rays) 1.56 vs 1.61, C5 (44K) 3.70 vs 3.40, C2 (57K) 6.82 vs
+            // 6.66 — one thread per ray pays only when short rays are plentiful.
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->m.device);
+            A->short_list = T.short_rays == 0 ? nullptr : leaf_buf + 2 * ns1;
+            A->short_min = T.short_rays == 1 ? 0 : 1000ll * sms;
+            A->walk2_min = T.walk2_min >= 0 ? T.walk2_min : 500ll * sms;
+            A->resume = leaf_buf + 3 * ns1;
+            A->leaves = leaf_buf + (3 + res_words) * ns1;
+            A->leaf_cap = cap;
         }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
-        if (leaf_buf && getenv("XB_PRINT_NCAND")) {  // diagnostics: candidate rays of k_walk + leaf histogram
-            const size_t ns = (size_t)n_local * 128;
-            std::vector<int32_t> lc(ns);
-            XB_CUDA(cudaMemcpyAsync(lc.data(), A->leaf_count, ns * 4, cudaMemcpyDeviceToHost, s));
-            XB_CUDA(cudaStreamSynchronize(s));
-            long long h[9] = {0};
-            for (int32_t v : lc) {
-                if (v & 0x40000000) { h[8]++; continue; }
-                const int c = v & 0x3fffffff;
-                h[c == 0 ? 0 : c <= 2 ? 1 : c <= 4 ? 2 : c <= 8 ? 3 : c <= 16 ? 4 : c <= 32 ? 5 : c <= 64 ? 6 : 7]++;
-            }
-            fprintf(stderr, "xb_render: %llu candidates; leaves 0:%lld 1-2:%lld 3-4:%lld 5-8:%lld 9-16:%lld "
-                            "17-32:%lld 33-64:%lld >64:%lld truncated:%lld\n",
-                    (unsigned long long)xb::read_scalar(A->walk_counter + 3, s), h[0], h[1], h[2], h[3], h[4],
-                    h[5], h[6], h[7], h[8]);
-        }
         if (A->dbg) {
             unsigned long long d[7];
             XB_CUDA(cudaMemcpyAsync(d, A->dbg, sizeof d, cudaMemcpyDeviceToHost, s));
@@ -768,14 +793,8 @@ static int run_rays(const xb_model* m, const xb_regions* r, int32_t field, const
         B->iflags = act->a.flags.p;
         fill_march(B->M, mp);
         B->mode = mode;
-        B->use_lbvh = 0;
-        {
-            const char* tr = getenv("XB_TRAVERSAL");
-            if (tr && strcmp(tr, "lbvh") == 0) {
-                B->use_lbvh = 1;
-                B->vlb = B->ilb = xb::active_lbvh(r->r, act->a, st.s).view();
-            }
-        }
+        B->use_lbvh = tuning_snapshot().traversal == 1;
+        if (B->use_lbvh) B->vlb = B->ilb = xb::active_lbvh(r->r, act->a, st.s).view();
         B->n = n;
         std::memcpy(B->tf, mp->tf_rgba, sizeof(B->tf));
         xb::DevBuf<double> dO, dD, d0, d1, dr, dout;

@@ -23,13 +23,6 @@ namespace xb {
 
 constexpr double kEpsWeight = 1e-12;     // EPS_WEIGHT, R/sampling.py:37
 
-// frame gather: 1 (default) = the reference's exact per-cell running sums, 0 = factored
-// trilinear sums with FMAs (within an ulp; see gather_shade).  Measured on C2 /
-// C3 (tools/ab.py, `make exact` + XB_LIB): 6.56 vs 6.61 / 1.597 vs 1.601 ms —
-// the dependent-add chain is not the limiter, so the exact sequence stays.
-#ifndef XB_EXACT_VALUE
-#define XB_EXACT_VALUE 1
-#endif
 constexpr double kTFar = 1.0e30;         // _T_FAR, R/render.py:49
 constexpr int kKdStack = 64;
 
@@ -93,10 +86,9 @@ struct SceneView {
     const float* __restrict__ vals;
     const RegionRec* __restrict__ rec;
     const int32_t* __restrict__ rids;
-    // brick records in region-list order (rb_a[i] = brick_a[rids[i]], same for
-    // rb_m): the frame gather reads a region's bricks without the id hop
-    const int4* __restrict__ rb_a;
-    const uint32_t* __restrict__ rb_m;
+    // frame-gather brick records in region-list order (rb[i] = brick rids[i]):
+    // a region's bricks are read without the id hop
+    const struct RbRec* __restrict__ rb;
     const KdNode* __restrict__ kd;
     const Kd4Node* __restrict__ kd4;
     int32_t root_lo[3], root_hi[3];
@@ -552,11 +544,11 @@ __device__ __forceinline__ void gather_fast(const SceneView& S, const int32_t* _
     }
 }
 
-// Frame-kernel gather (k_warp): the value sums num/den are the reference's
-// exact FP64 sequence (as gather_fast); the analytic gradient, which only feeds
-// the headlight shading factor (R/render.py:284-289, never alpha, positions
-// or counters), is evaluated in FP32 with the trilinear sums factored per
-// axis.  Per brick, with the hat factors of invalid window cells zeroed,
+// Frame-kernel gather (k_warp, k_short): the value sums num/den are the
+// reference's exact FP64 sequence; the analytic gradient, which only feeds the
+// headlight shading factor (R/render.py:284-289, never alpha, positions or
+// counters), is evaluated in FP32 with the trilinear sums factored per axis.
+// Per brick, with the hat factors of invalid window cells zeroed,
 //   gnum = sum hx hy hz u,  dn_x = sum sx hy hz u, ...,  dd_x = (sum sx)(sum hy)(sum hz), ...
 // where u = v - v0 (v0 = first contributing cell, R/sampling.py:160-170), so a
 // locally constant field still yields an exactly zero gradient (shade 0.2).
@@ -567,6 +559,29 @@ struct FastAccum {
     float g[3];
     int n_nz;
 };
+
+// Brick record of the frame gather, in region-list order (one per entry of
+// RegionSet.brick_ids): the lower corner as FP64 (no integer->FP64 conversion
+// per sample: the conversion unit, not the FP64 pipe, limited the round-1
+// gather), the scalar offset, and level | nx<<5 | ny<<14 | nz<<23.  32 B, two
+// 16-B loads, read by every lane of a warp at the same address (broadcast).
+struct __align__(16) RbRec {
+    double lx, ly, lz;
+    uint32_t off, meta;
+};
+static_assert(sizeof(RbRec) == 32, "RbRec is 32 bytes");
+
+__device__ __forceinline__ RbRec load_rb(const RbRec* __restrict__ p) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const int4 b = __ldg(reinterpret_cast<const int4*>(p) + 1);
+    RbRec r;
+    r.lx = a.x;
+    r.ly = a.y;
+    r.lz = __hiloint2double(b.y, b.x);
+    r.off = (uint32_t)b.z;
+    r.meta = (uint32_t)b.w;
+    return r;
+}
 
 // Running state of the frame gather of one sample (value sums in the
 // reference's exact FP64 sequence; FP32 shading-gradient partials).
@@ -589,106 +604,101 @@ struct ShadeAcc {
     }
 };
 
-// one brick of the frame gather: adds brick b's window cells to A
+// One axis of a brick's 2-cell window (R/sampling.py:90-100, _hat_terms 57-63):
+// x0 = floor((p - l)/w - 0.5); cell centres c = l + (x + 0.5) w; hats
+// 1 - |c - p|/w.  Division by the power-of-two width is an exact scaling, so
+// each fused multiply-add below rounds exactly once where the reference's
+// unfused code rounds once (the product is exact): bit-identical values.
+// The floor comes from one conversion (cvt.rmi) and the centre from the
+// integer back in FP64 — two conversion-unit ops per axis (round 1: four).
+struct Axis2 {
+    double h0, h1;  // hats of slots x0, x0 + 1, zeroed when the slot is invalid
+    int x0;
+    bool v0, v1;    // slot inside the brick and hat > 0 (the reference's h > 0 test)
+    float s0, s1;   // gradient slopes: sign(c - p) / w, zeroed when invalid
+};
+
+__device__ __forceinline__ Axis2 window_axis(double p, double l, int n, double w, double iw, float fw) {
+    Axis2 A;
+    const double t = __fma_rn(p - l, iw, -0.5);
+    A.x0 = __double2int_rd(t);
+    const double c0 = __fma_rn((double)A.x0 + 0.5, w, l);  // exact: l + (x0 + 1/2) w
+    const double e0 = c0 - p, e1 = (c0 + w) - p;
+    const double h0 = __fma_rn(-fabs(e0), iw, 1.0), h1 = __fma_rn(-fabs(e1), iw, 1.0);
+    A.v0 = (unsigned)A.x0 < (unsigned)n && h0 > 0.0;
+    A.v1 = (unsigned)(A.x0 + 1) < (unsigned)n && h1 > 0.0;
+    A.h0 = A.v0 ? h0 : 0.0;
+    A.h1 = A.v1 ? h1 : 0.0;
+    A.s0 = A.v0 ? (e0 > 0.0 ? fw : -fw) : 0.f;
+    A.s1 = A.v1 ? (e1 > 0.0 ? fw : -fw) : 0.f;
+    return A;
+}
+
+// one brick of the frame gather: adds brick b's window cells to A.  Every
+// listed brick's support holds the whole region (ABR construction), so the
+// window always overlaps the brick; invalid slots get zero hats (a skipped
+// term adds +0 / +-0, leaving the running sums bit-identical) and clamped,
+// in-brick load indices, so the 8 cells run branch-free.
 template <bool GRAD>
-__device__ __forceinline__ void brick_step(const SceneView& S, const int4 ba, const uint32_t bm, double px, double py,
-                                           double pz, ShadeAcc& A) {
-    const int lev = bm & 31;
-    const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
-    const double w = pow2(lev), iw_d = pow2(-lev);
-    const double fx = floor((px - (double)ba.x) * iw_d - 0.5);
-    const double fy = floor((py - (double)ba.y) * iw_d - 0.5);
-    const double fz = floor((pz - (double)ba.z) * iw_d - 0.5);
-    if (!(fx >= -1.0 && fx < (double)nx && fy >= -1.0 && fy < (double)ny && fz >= -1.0 && fz < (double)nz)) return;
-    const int x0 = (int)fx, y0 = (int)fy, z0 = (int)fz;
-    const double half = 0.5 * w;
-    const double cx0 = (double)(ba.x + x0 * (1 << lev)) + half, cx1 = cx0 + w;
-    const double cy0 = (double)(ba.y + y0 * (1 << lev)) + half, cy1 = cy0 + w;
-    const double cz0 = (double)(ba.z + z0 * (1 << lev)) + half, cz1 = cz0 + w;
-    const double ex0 = cx0 - px, ex1 = cx1 - px, ey0 = cy0 - py, ey1 = cy1 - py, ez0 = cz0 - pz, ez1 = cz1 - pz;
-    double hx0 = 1.0 - fabs(ex0) * iw_d, hx1 = 1.0 - fabs(ex1) * iw_d;
-    double hy0 = 1.0 - fabs(ey0) * iw_d, hy1 = 1.0 - fabs(ey1) * iw_d;
-    double hz0 = 1.0 - fabs(ez0) * iw_d, hz1 = 1.0 - fabs(ez1) * iw_d;
-    // A window cell contributes iff its three axis slots are valid (inside
-    // the brick, hat > 0).  Zeroing the hat of an invalid slot turns every
-    // skipped term into +0 (h) and +-0 (h*v), which leave the running sums
-    // bit-identical, so the 8 cells run branch-free; loads use clamped,
-    // in-brick indices.
-    const bool vx0 = x0 >= 0 && hx0 > 0.0, vx1 = x0 + 1 < nx && hx1 > 0.0;
-    const bool vy0 = y0 >= 0 && hy0 > 0.0, vy1 = y0 + 1 < ny && hy1 > 0.0;
-    const bool vz0 = z0 >= 0 && hz0 > 0.0, vz1 = z0 + 1 < nz && hz1 > 0.0;
-    hx0 = vx0 ? hx0 : 0.0; hx1 = vx1 ? hx1 : 0.0;
-    hy0 = vy0 ? hy0 : 0.0; hy1 = vy1 ? hy1 : 0.0;
-    hz0 = vz0 ? hz0 : 0.0; hz1 = vz1 ? hz1 : 0.0;
-    const int ncx = (int)vx0 + (int)vx1, ncy = (int)vy0 + (int)vy1, ncz = (int)vz0 + (int)vz1;
-    A.n_nz += ncx * ncy * ncz;
-    const int xa = max(x0, 0), xb = min(x0 + 1, nx - 1);
-    const int ya = max(y0, 0), yb = min(y0 + 1, ny - 1);
-    const int za = max(z0, 0), zb = min(z0 + 1, nz - 1);
-    const float* __restrict__ base = S.vals + (uint32_t)ba.w;
+__device__ __forceinline__ void brick_step(const SceneView& S, const RbRec& B, double px, double py, double pz,
+                                           ShadeAcc& A) {
+    const int lev = B.meta & 31;
+    const int nx = (B.meta >> 5) & 511, ny = (B.meta >> 14) & 511, nz = (B.meta >> 23) & 511;
+    const double w = pow2(lev), iw = pow2(-lev);
+    const float fw = __int_as_float((127 - lev) << 23);  // 1/w in FP32
+    const Axis2 X = window_axis(px, B.lx, nx, w, iw, fw);
+    const Axis2 Y = window_axis(py, B.ly, ny, w, iw, fw);
+    const Axis2 Z = window_axis(pz, B.lz, nz, w, iw, fw);
+    A.n_nz += ((int)X.v0 + (int)X.v1) * ((int)Y.v0 + (int)Y.v1) * ((int)Z.v0 + (int)Z.v1);
+    const int xa = max(X.x0, 0), xb = min(X.x0 + 1, nx - 1);
+    const int ya = max(Y.x0, 0), yb = min(Y.x0 + 1, ny - 1);
+    const int za = max(Z.x0, 0), zb = min(Z.x0 + 1, nz - 1);
+    const float* __restrict__ base = S.vals + B.off;
     const int r00 = nx * (ya + ny * za), r01 = nx * (yb + ny * za), r10 = nx * (ya + ny * zb),
               r11 = nx * (yb + ny * zb);
     float vv[2][2][2];  // [dz][dy][dx]
-    // 32-bit in-brick offsets: one 64-bit base, then a scaled add per load
     vv[0][0][0] = __ldg(base + (r00 + xa)); vv[0][0][1] = __ldg(base + (r00 + xb));
     vv[0][1][0] = __ldg(base + (r01 + xa)); vv[0][1][1] = __ldg(base + (r01 + xb));
     vv[1][0][0] = __ldg(base + (r10 + xa)); vv[1][0][1] = __ldg(base + (r10 + xb));
     vv[1][1][0] = __ldg(base + (r11 + xa)); vv[1][1][1] = __ldg(base + (r11 + xb));
-#if XB_EXACT_VALUE
-    const double hxy00 = hx0 * hy0, hxy01 = hx1 * hy0, hxy10 = hx0 * hy1, hxy11 = hx1 * hy1;  // [dy][dx]
-    const double hzz[2] = {hz0, hz1};
+    // the reference's sequence: h = (hx*hy)*hz, cells z, y, x ascending
+    const double hxy00 = X.h0 * Y.h0, hxy01 = X.h1 * Y.h0, hxy10 = X.h0 * Y.h1, hxy11 = X.h1 * Y.h1;  // [dy][dx]
+    const double hzz[2] = {Z.h0, Z.h1};
 #pragma unroll
-    for (int dz = 0; dz < 2; dz++) {  // z, y, x ascending: the reference's order
+    for (int dz = 0; dz < 2; dz++) {
         const double h0 = hxy00 * hzz[dz], h1 = hxy01 * hzz[dz], h2 = hxy10 * hzz[dz], h3 = hxy11 * hzz[dz];
         A.num += h0 * (double)vv[dz][0][0]; A.den += h0;
         A.num += h1 * (double)vv[dz][0][1]; A.den += h1;
         A.num += h2 * (double)vv[dz][1][0]; A.den += h2;
         A.num += h3 * (double)vv[dz][1][1]; A.den += h3;
     }
-#else
-    // Factored trilinear sums (the reference's 8-term running sums
-    // reassociated, FP64 with fused multiply-adds): num_b = sum_z hz sum_y hy
-    // sum_x hx v, den_b = (sum hx)(sum hy)(sum hz).  Within an ulp of the
-    // reference's sequence and a quarter of its dependent-add chain.
-    const double x00 = __fma_rn(hx1, (double)vv[0][0][1], hx0 * (double)vv[0][0][0]);
-    const double x01 = __fma_rn(hx1, (double)vv[0][1][1], hx0 * (double)vv[0][1][0]);
-    const double x10 = __fma_rn(hx1, (double)vv[1][0][1], hx0 * (double)vv[1][0][0]);
-    const double x11 = __fma_rn(hx1, (double)vv[1][1][1], hx0 * (double)vv[1][1][0]);
-    const double yz0 = __fma_rn(hy1, x01, hy0 * x00), yz1 = __fma_rn(hy1, x11, hy0 * x10);
-    A.num = __fma_rn(hz1, yz1, __fma_rn(hz0, yz0, A.num));
-    A.den = __fma_rn((hx0 + hx1) * (hy0 + hy1), hz0 + hz1, A.den);
-#endif
     if (GRAD) {
-        if (!A.have_ref && ncx * ncy * ncz > 0) {  // first contributing cell (z, y, x order)
-            const float r0 = vx0 ? vv[0][0][0] : vv[0][0][1], r1 = vx0 ? vv[0][1][0] : vv[0][1][1];
-            const float r2 = vx0 ? vv[1][0][0] : vv[1][0][1], r3 = vx0 ? vv[1][1][0] : vv[1][1][1];
-            const float p0 = vy0 ? r0 : r1, p1 = vy0 ? r2 : r3;
-            A.v0 = vz0 ? p0 : p1;  // select chain: no local-memory indexing
+        if (!A.have_ref && (X.v0 || X.v1) && (Y.v0 || Y.v1) && (Z.v0 || Z.v1)) {  // first contributing cell
+            const float r0 = X.v0 ? vv[0][0][0] : vv[0][0][1], r1 = X.v0 ? vv[0][1][0] : vv[0][1][1];
+            const float r2 = X.v0 ? vv[1][0][0] : vv[1][0][1], r3 = X.v0 ? vv[1][1][0] : vv[1][1][1];
+            const float p0 = Y.v0 ? r0 : r1, p1 = Y.v0 ? r2 : r3;
+            A.v0 = Z.v0 ? p0 : p1;  // select chain: no local-memory indexing
             A.have_ref = true;
         }
-        const float fw = (float)iw_d;
-        const float ax0 = (float)hx0, ax1 = (float)hx1, ay0 = (float)hy0, ay1 = (float)hy1, az0 = (float)hz0,
-                    az1 = (float)hz1;
-        const float sx0 = vx0 ? (ex0 > 0.0 ? fw : -fw) : 0.f, sx1 = vx1 ? (ex1 > 0.0 ? fw : -fw) : 0.f;
-        const float sy0 = vy0 ? (ey0 > 0.0 ? fw : -fw) : 0.f, sy1 = vy1 ? (ey1 > 0.0 ? fw : -fw) : 0.f;
-        const float sz0 = vz0 ? (ez0 > 0.0 ? fw : -fw) : 0.f, sz1 = vz1 ? (ez1 > 0.0 ? fw : -fw) : 0.f;
+        const float ax0 = (float)X.h0, ax1 = (float)X.h1, ay0 = (float)Y.h0, ay1 = (float)Y.h1,
+                    az0 = (float)Z.h0, az1 = (float)Z.h1;
         float C[2], D[2], E[2];
 #pragma unroll
         for (int dz = 0; dz < 2; dz++) {
             const float u00 = vv[dz][0][0] - A.v0, u01 = vv[dz][0][1] - A.v0;
             const float u10 = vv[dz][1][0] - A.v0, u11 = vv[dz][1][1] - A.v0;
-            const float A0 = fmaf(ax1, u01, ax0 * u00), A1 = fmaf(ax1, u11, ax0 * u10);  // x-hat reductions
-            const float B0 = fmaf(sx1, u01, sx0 * u00), B1 = fmaf(sx1, u11, sx0 * u10);  // x-slope reductions
+            const float A0 = fmaf(ax1, u01, ax0 * u00), A1 = fmaf(ax1, u11, ax0 * u10);      // x-hat reductions
+            const float B0 = fmaf(X.s1, u01, X.s0 * u00), B1 = fmaf(X.s1, u11, X.s0 * u10);  // x-slope reductions
             C[dz] = fmaf(ay1, A1, ay0 * A0);  // sum hx hy u
             D[dz] = fmaf(ay1, B1, ay0 * B0);  // sum sx hy u
-            E[dz] = fmaf(sy1, A1, sy0 * A0);  // sum hx sy u
+            E[dz] = fmaf(Y.s1, A1, Y.s0 * A0);  // sum hx sy u
         }
         A.gnum = fmaf(az1, C[1], fmaf(az0, C[0], A.gnum));
         A.dn0 = fmaf(az1, D[1], fmaf(az0, D[0], A.dn0));
         A.dn1 = fmaf(az1, E[1], fmaf(az0, E[0], A.dn1));
-        A.dn2 = fmaf(sz1, C[1], fmaf(sz0, C[0], A.dn2));
+        A.dn2 = fmaf(Z.s1, C[1], fmaf(Z.s0, C[0], A.dn2));
         const float Hx = ax0 + ax1, Hy = ay0 + ay1, Hz = az0 + az1;
-        const float Sx = sx0 + sx1, Sy = sy0 + sy1, Sz = sz0 + sz1;
+        const float Sx = X.s0 + X.s1, Sy = Y.s0 + Y.s1, Sz = Z.s0 + Z.s1;
         A.fden = fmaf(Hx * Hy, Hz, A.fden);
         A.dd0 = fmaf(Sx * Hy, Hz, A.dd0);
         A.dd1 = fmaf(Hx * Sy, Hz, A.dd1);
@@ -696,199 +706,18 @@ __device__ __forceinline__ void brick_step(const SceneView& S, const int4 ba, co
     }
 }
 
-// the frame gather over region-list entries [off, off + nids) (S.rb_a / rb_m)
+// the frame gather over region-list entries [off, off + nids) (S.rb)
 template <bool GRAD>
 __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, int nids, double px, double py,
                                              double pz, FastAccum& F) {
     ShadeAcc A;
     A.clear();
-    const int4* __restrict__ ra = S.rb_a + off;
-    const uint32_t* __restrict__ rm = S.rb_m + off;
-    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, __ldg(ra + t), __ldg(rm + t), px, py, pz, A);
+    const RbRec* __restrict__ rb = S.rb + off;
+    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, load_rb(rb + t), px, py, pz, A);
     F.num = A.num;
     F.den = A.den;
     F.n_nz = A.n_nz;
     if (GRAD) A.gradient(F.g);
-}
-
-// ---------------------------------------------------------------------------
-// Chunk gather for k_warp: the (sample, brick) pairs of a 32-sample chunk are
-// flattened across the warp, so every lane reconstructs one brick per round
-// whatever the brick counts of the samples (regions hold 1..8+ bricks, which
-// left half the lanes idle in a per-sample brick loop).  Each pair yields the
-// brick's partial sums (the reference's per-cell sequence, started from 0);
-// the sample's lane then adds its partials in ascending brick order.  This
-// reassociates the reference's single running sum across brick boundaries
-// (R/sampling.py:66-103), so num/den may differ from it in the last ulp; no
-// test threshold, counter or image tolerance is sensitive to that.
-
-struct BrickPart {
-    double num, den;
-    float fden, gnum, dn0, dn1, dn2, dd0, dd1, dd2;
-    float v0;      // first contributing cell of the brick (gradient shift)
-    int nnz;       // contributing cells; 0: brick contributes nothing
-    float pad[2];
-};
-static_assert(sizeof(BrickPart) == 64, "BrickPart is 64 bytes");
-
-template <bool GRAD>
-__device__ __forceinline__ void brick_part(const SceneView& S, const int4 ba, const uint32_t bm, double px, double py,
-                                           double pz, BrickPart& P) {
-    P.num = 0.0;
-    P.den = 0.0;
-    P.nnz = 0;
-    P.fden = P.gnum = P.dn0 = P.dn1 = P.dn2 = P.dd0 = P.dd1 = P.dd2 = 0.f;
-    P.v0 = 0.f;
-    const int lev = bm & 31;
-    const int nx = (bm >> 5) & 511, ny = (bm >> 14) & 511, nz = (bm >> 23) & 511;
-    const double w = pow2(lev), iw_d = pow2(-lev);
-    const double fx = floor((px - (double)ba.x) * iw_d - 0.5);
-    const double fy = floor((py - (double)ba.y) * iw_d - 0.5);
-    const double fz = floor((pz - (double)ba.z) * iw_d - 0.5);
-    if (!(fx >= -1.0 && fx < (double)nx && fy >= -1.0 && fy < (double)ny && fz >= -1.0 && fz < (double)nz)) return;
-    const int x0 = (int)fx, y0 = (int)fy, z0 = (int)fz;
-    const double half = 0.5 * w;
-    const double cx0 = (double)(ba.x + x0 * (1 << lev)) + half, cx1 = cx0 + w;
-    const double cy0 = (double)(ba.y + y0 * (1 << lev)) + half, cy1 = cy0 + w;
-    const double cz0 = (double)(ba.z + z0 * (1 << lev)) + half, cz1 = cz0 + w;
-    const double ex0 = cx0 - px, ex1 = cx1 - px, ey0 = cy0 - py, ey1 = cy1 - py, ez0 = cz0 - pz, ez1 = cz1 - pz;
-    double hx0 = 1.0 - fabs(ex0) * iw_d, hx1 = 1.0 - fabs(ex1) * iw_d;
-    double hy0 = 1.0 - fabs(ey0) * iw_d, hy1 = 1.0 - fabs(ey1) * iw_d;
-    double hz0 = 1.0 - fabs(ez0) * iw_d, hz1 = 1.0 - fabs(ez1) * iw_d;
-    // invalid window slots (outside the brick, hat <= 0) get a zero hat: their
-    // terms are +0 / +-0 and leave the running sums bit-identical
-    const bool vx0 = x0 >= 0 && hx0 > 0.0, vx1 = x0 + 1 < nx && hx1 > 0.0;
-    const bool vy0 = y0 >= 0 && hy0 > 0.0, vy1 = y0 + 1 < ny && hy1 > 0.0;
-    const bool vz0 = z0 >= 0 && hz0 > 0.0, vz1 = z0 + 1 < nz && hz1 > 0.0;
-    hx0 = vx0 ? hx0 : 0.0; hx1 = vx1 ? hx1 : 0.0;
-    hy0 = vy0 ? hy0 : 0.0; hy1 = vy1 ? hy1 : 0.0;
-    hz0 = vz0 ? hz0 : 0.0; hz1 = vz1 ? hz1 : 0.0;
-    P.nnz = ((int)vx0 + (int)vx1) * ((int)vy0 + (int)vy1) * ((int)vz0 + (int)vz1);
-    const int xa = max(x0, 0), xb = min(x0 + 1, nx - 1);
-    const int ya = max(y0, 0), yb = min(y0 + 1, ny - 1);
-    const int za = max(z0, 0), zb = min(z0 + 1, nz - 1);
-    const float* __restrict__ base = S.vals + (uint32_t)ba.w;
-    const int r00 = nx * (ya + ny * za), r01 = nx * (yb + ny * za), r10 = nx * (ya + ny * zb),
-              r11 = nx * (yb + ny * zb);
-    float vv[2][2][2];  // [dz][dy][dx]
-    vv[0][0][0] = __ldg(base + r00 + xa); vv[0][0][1] = __ldg(base + r00 + xb);
-    vv[0][1][0] = __ldg(base + r01 + xa); vv[0][1][1] = __ldg(base + r01 + xb);
-    vv[1][0][0] = __ldg(base + r10 + xa); vv[1][0][1] = __ldg(base + r10 + xb);
-    vv[1][1][0] = __ldg(base + r11 + xa); vv[1][1][1] = __ldg(base + r11 + xb);
-    const double hxy00 = hx0 * hy0, hxy01 = hx1 * hy0, hxy10 = hx0 * hy1, hxy11 = hx1 * hy1;  // [dy][dx]
-    double num = 0.0, den = 0.0;
-#pragma unroll
-    for (int dz = 0; dz < 2; dz++) {  // z, y, x ascending: the reference's order
-        const double hz = dz ? hz1 : hz0;
-        const double h0 = hxy00 * hz, h1 = hxy01 * hz, h2 = hxy10 * hz, h3 = hxy11 * hz;
-        num += h0 * (double)vv[dz][0][0]; den += h0;
-        num += h1 * (double)vv[dz][0][1]; den += h1;
-        num += h2 * (double)vv[dz][1][0]; den += h2;
-        num += h3 * (double)vv[dz][1][1]; den += h3;
-    }
-    P.num = num;
-    P.den = den;
-    if (GRAD && P.nnz > 0) {
-        const float r0 = vx0 ? vv[0][0][0] : vv[0][0][1], r1 = vx0 ? vv[0][1][0] : vv[0][1][1];
-        const float r2 = vx0 ? vv[1][0][0] : vv[1][0][1], r3 = vx0 ? vv[1][1][0] : vv[1][1][1];
-        const float q0 = vy0 ? r0 : r1, q1 = vy0 ? r2 : r3;
-        const float v0 = vz0 ? q0 : q1;  // first contributing cell (z, y, x order)
-        P.v0 = v0;
-        const float fw = (float)iw_d;
-        const float ax0 = (float)hx0, ax1 = (float)hx1, ay0 = (float)hy0, ay1 = (float)hy1, az0 = (float)hz0,
-                    az1 = (float)hz1;
-        const float sx0 = vx0 ? (ex0 > 0.0 ? fw : -fw) : 0.f, sx1 = vx1 ? (ex1 > 0.0 ? fw : -fw) : 0.f;
-        const float sy0 = vy0 ? (ey0 > 0.0 ? fw : -fw) : 0.f, sy1 = vy1 ? (ey1 > 0.0 ? fw : -fw) : 0.f;
-        const float sz0 = vz0 ? (ez0 > 0.0 ? fw : -fw) : 0.f, sz1 = vz1 ? (ez1 > 0.0 ? fw : -fw) : 0.f;
-        float C[2], D[2], E[2];
-#pragma unroll
-        for (int dz = 0; dz < 2; dz++) {
-            const float u00 = vv[dz][0][0] - v0, u01 = vv[dz][0][1] - v0;
-            const float u10 = vv[dz][1][0] - v0, u11 = vv[dz][1][1] - v0;
-            const float A0 = fmaf(ax1, u01, ax0 * u00), A1 = fmaf(ax1, u11, ax0 * u10);
-            const float B0 = fmaf(sx1, u01, sx0 * u00), B1 = fmaf(sx1, u11, sx0 * u10);
-            C[dz] = fmaf(ay1, A1, ay0 * A0);  // sum hx hy u
-            D[dz] = fmaf(ay1, B1, ay0 * B0);  // sum sx hy u
-            E[dz] = fmaf(sy1, A1, sy0 * A0);  // sum hx sy u
-        }
-        P.gnum = fmaf(az1, C[1], az0 * C[0]);
-        P.dn0 = fmaf(az1, D[1], az0 * D[0]);
-        P.dn1 = fmaf(az1, E[1], az0 * E[0]);
-        P.dn2 = fmaf(sz1, C[1], sz0 * C[0]);
-        const float Hx = ax0 + ax1, Hy = ay0 + ay1, Hz = az0 + az1;
-        const float Sx = sx0 + sx1, Sy = sy0 + sy1, Sz = sz0 + sz1;
-        P.fden = Hx * Hy * Hz;
-        P.dd0 = Sx * Hy * Hz;
-        P.dd1 = Hx * Sy * Hz;
-        P.dd2 = Hx * Hy * Sz;
-    }
-}
-
-// All 32 lanes call this together; lanes with act hold one sample each.
-template <bool GRAD>
-__device__ __forceinline__ void gather_chunk(const SceneView& S, bool act, int ids_off, int nids, double px, double py,
-                                             double pz, BrickPart* __restrict__ scratch, int lane, FastAccum& F) {
-    const unsigned FULL = 0xffffffffu;
-    const int nb = act ? nids : 0;
-    int Qi = nb;  // inclusive prefix of the brick counts
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(FULL, Qi, o);
-        if (lane >= o) Qi += v;
-    }
-    const int I = __shfl_sync(FULL, Qi, 31);
-    const int Qe = Qi - nb;
-    F.num = 0.0;
-    F.den = 0.0;
-    F.n_nz = 0;
-    float fden = 0.f, gnum = 0.f, dn0 = 0.f, dn1 = 0.f, dn2 = 0.f, dd0 = 0.f, dd1 = 0.f, dd2 = 0.f, v0 = 0.f;
-    bool have = false;
-    for (int base = 0; base < I; base += 32) {
-        const int q = base + lane;
-        int j = 0;  // owner sample: #{lanes with Qi <= q}
-#pragma unroll
-        for (int b = 16; b >= 1; b >>= 1) {
-            const int v = __shfl_sync(FULL, Qi, j + b - 1);
-            if (v <= q) j += b;
-        }
-        j = min(j, 31);
-        const double qx = __shfl_sync(FULL, px, j), qy = __shfl_sync(FULL, py, j), qz = __shfl_sync(FULL, pz, j);
-        const int qe = __shfl_sync(FULL, Qe, j), qoff = __shfl_sync(FULL, ids_off, j);
-        BrickPart P;
-        if (q < I) {
-            const int64_t e = (int64_t)qoff + (q - qe);
-            brick_part<GRAD>(S, __ldg(S.rb_a + e), __ldg(S.rb_m + e), qx, qy, qz, P);
-        } else {
-            P.num = P.den = 0.0;
-            P.nnz = 0;
-            P.fden = P.gnum = P.dn0 = P.dn1 = P.dn2 = P.dd0 = P.dd1 = P.dd2 = P.v0 = 0.f;
-        }
-        scratch[lane] = P;
-        __syncwarp();
-        const int k0 = max(Qe, base) - base, k1 = min(Qi, base + 32) - base;
-        for (int k = k0; k < k1; k++) {  // my bricks of this round, ascending
-            const BrickPart& B = scratch[k];
-            F.num += B.num;
-            F.den += B.den;
-            F.n_nz += B.nnz;
-            if (GRAD && B.nnz > 0) {
-                if (!have) { v0 = B.v0; have = true; }
-                const float sh = B.v0 - v0;  // re-reference the brick's partials to v0
-                gnum += fmaf(sh, B.fden, B.gnum);
-                dn0 += fmaf(sh, B.dd0, B.dn0);
-                dn1 += fmaf(sh, B.dd1, B.dn1);
-                dn2 += fmaf(sh, B.dd2, B.dn2);
-                dd0 += B.dd0; dd1 += B.dd1; dd2 += B.dd2;
-                fden += B.fden;
-            }
-        }
-        __syncwarp();
-    }
-    if (GRAD) {
-        F.g[0] = dn0 * fden - gnum * dd0;
-        F.g[1] = dn1 * fden - gnum * dd1;
-        F.g[2] = dn2 * fden - gnum * dd2;
-    }
 }
 
 // _shade_factor (R/render.py:284-289) on an unnormalised FP32 gradient direction

@@ -1,17 +1,12 @@
 // render.cu — the fused sm_100a ray-march kernels (paper §4-5) and the
 // single-ray batch kernel behind integrate_ray / iso_intersect.
 //
-// k_frame (default): persistent warps.  Rays of one frame are "slots" in
-// screen-tile order (16x8 tiles, 8x4 per warp chunk); a warp grabs 32 slots at
-// a time from a global counter and every lane whose ray finished takes the
-// next slot at once, so lanes stay busy although rays differ ~10x in length
-// (visits per ray p50 36 / p99 186).  Each loop iteration a lane
-// (1) finishes its region and fetches the next one from the ordered k-d walk,
-// (2) refills with a new ray if its ray ended, (3) takes exactly one sample,
-// so the expensive gather runs with (nearly) all lanes converged.
-//
-// k_render: one thread per pixel, one block per tile — kept as the simple
-// reference kernel (XB_KERNEL=tile) for A/B measurements.
+// Frame pipeline: k_classify -> CUB hit select -> k_walk ->
+// k_route -> k_walk2 -> k_warp (warp per long ray, then a lane per short
+// ray); iso scenes run the same chain on the iso set first, ending in
+// k_iso_warp.  k_render: one thread per pixel, one block per tile — the
+// kernel of the per-visit LBVH traversal and the cell-location gather
+// (tuning.kernel = 1 runs every frame through it).
 //
 // The per-pixel arithmetic is `_render_kernel` (R/render.py:521-578) in both.
 #include <cmath>
@@ -113,225 +108,6 @@ __global__ void __launch_bounds__(128) k_iso_pass(const __grid_constant__ Render
 }
 
 // ---------------------------------------------------------------------------
-// persistent frame kernel
-
-struct LaneState {
-    Ray r;
-    KdWalk w;
-    double rho, tmax;
-    double acc[4];
-    // current region
-    const int32_t* ids;
-    int nids, rid;
-    double dt, s1, t_out, prev, k;
-    // next region (found by the pipelined walk), query start of the walk
-    int nrid;
-    double nci, nco, q_t;
-    int64_t slot, out;
-    int nreg, nsmp;
-};
-
-enum : int { kSearching = 0, kFound = 1, kExhausted = 2 };
-
-template <int GRAD, bool ISO, bool COUNT, int KSTEPS = kKdSteps, int MINB = kFrameMinBlocks>
-__global__ void __launch_bounds__(kFrameThreads, MINB) k_frame(const __grid_constant__ RenderArgs A, int64_t n_slots) {
-    __shared__ double s_tf[1024];
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
-    __syncthreads();
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-
-    LaneState L;
-    bool has_ray = false, in_region = false, early = false;
-    int nstate = kExhausted;
-    int64_t chunk_next = 0, chunk_left = 0;
-    bool exhausted = false;
-    unsigned long long tot_reg = 0, tot_smp = 0, tot_bytes = 0;
-    Accum G;
-
-    for (;;) {
-        // ---- prefetch the k-d node the walk visits this iteration (its latency
-        //      hides behind the sample's gather)
-        KdNode nd = {0, 0};
-        uint8_t fl = 0;
-        bool pre = has_ray && nstate == kSearching && L.w.node >= 0;  // cleared when the lane gets a new ray
-        if (pre) {
-            nd = A.S.kd[L.w.node];
-            fl = A.vflags[L.w.node];
-        }
-        // ---- (1) promote the prefetched next region / finish the ray
-        if (has_ray && !in_region) {
-            if (!early && nstate == kFound) {
-                const RegionRec rr = A.S.rec[L.nrid];
-                L.rid = L.nrid;
-                L.nids = rr.meta & 0xffffff;
-                L.ids = A.S.rids + rr.ids_begin;
-                const double fw = pow2(rr.meta >> 24);
-                L.dt = fw / (A.M.spc * A.M.rate);
-                L.s1 = fw / A.M.spc;
-                L.t_out = L.nco;
-                L.prev = L.nci;
-                L.k = floor(L.nci / L.dt - L.rho) + 1.0;
-                L.nreg++;
-                if (COUNT) tot_bytes += 32 + 4 * (unsigned long long)L.nids;
-                in_region = true;
-                // the reference's next query: t = restart(t_out); stop if t >= tmax
-                L.q_t = restart_t(L.nco);
-                nstate = L.q_t >= L.tmax ? kExhausted : kSearching;
-            } else if (early || nstate == kExhausted) {
-                if (ISO) {
-                    const double f = A.iso_shade[L.slot];
-                    if (f >= 0.0) {
-                        const double wgt = 1.0 - L.acc[3];
-                        L.acc[0] += wgt * A.M.iso_rgb[0] * f;
-                        L.acc[1] += wgt * A.M.iso_rgb[1] * f;
-                        L.acc[2] += wgt * A.M.iso_rgb[2] * f;
-                        L.acc[3] = 1.0;
-                    }
-                }
-                write_pixel(A, L.out, L.acc, L.nreg, L.nsmp);
-                tot_reg += L.nreg;
-                tot_smp += L.nsmp;
-                has_ray = false;
-            }
-        }
-        // ---- (2) refill: lanes without a ray take the next slots of the warp's chunk
-        bool want = !has_ray;
-        unsigned need = __ballot_sync(FULL, want && !exhausted);
-        while (need) {
-            if (chunk_left == 0) {
-                unsigned long long b = 0;
-                if (lane == 0) b = atomicAdd(A.work_counter, 32ull);
-                b = __shfl_sync(FULL, b, 0);
-                chunk_next = (int64_t)b;
-                chunk_left = (int64_t)b < n_slots ? min((int64_t)32, n_slots - (int64_t)b) : 0;
-                if (chunk_left == 0) { exhausted = true; break; }
-            }
-            const int rank = __popc(need & lt_mask);
-            const bool mine = want && rank < chunk_left;
-            const int took = min(__popc(need), (int)chunk_left);
-            const int64_t slot = chunk_next + rank;
-            chunk_next += took;
-            chunk_left -= took;
-            if (mine) {
-                const SlotPix sp = slot_pixel(A, slot);
-                if (sp.live) {
-                    pixel_ray(A, sp.x, sp.y, L.r);
-                    L.rho = rho_hash((uint64_t)sp.pix, A.M.seed);
-                    double tmin = 0.0, tmax = kTFar;
-                    clip_ray(A.M, L.r, tmin, tmax);
-                    L.slot = slot;
-                    L.out = sp.out;
-                    L.acc[0] = L.acc[1] = L.acc[2] = L.acc[3] = 0.0;
-                    L.nreg = 0;
-                    L.nsmp = 0;
-                    if (tmin >= tmax) {
-                        write_pixel(A, sp.out, L.acc, 0, 0);
-                    } else {
-                        L.tmax = ISO ? A.iso_tend[slot] : tmax;
-                        L.q_t = tmin;
-                        kd_begin(A.S, L.r, L.w);
-                        pre = false;  // the prefetched node belonged to the previous ray
-                        has_ray = true;
-                        in_region = false;
-                        early = false;
-                        nstate = kSearching;
-                    }
-                }
-                want = !has_ray;
-            }
-            need = __ballot_sync(FULL, want && !exhausted);
-        }
-        if (!__any_sync(FULL, has_ray)) {
-            if (exhausted) break;
-            continue;
-        }
-        // ---- (3) one sample (midpoint of the next lattice interval, R/render.py:406-449)
-        if (in_region) {
-            double tk;
-            bool last = false;
-            for (;;) {
-                tk = L.dt * (L.k + L.rho);
-                L.k += 1.0;
-                if (tk >= L.t_out) { tk = L.t_out; last = true; break; }
-                if (tk > L.prev) break;
-            }
-            const double sl = tk - L.prev;
-            const double mid = 0.5 * (L.prev + tk);
-            L.prev = tk;
-            L.nsmp++;
-            const double px = L.r.o[0] + mid * L.r.d[0], py = L.r.o[1] + mid * L.r.d[1], pz = L.r.o[2] + mid * L.r.d[2];
-            gather_fast<GRAD == 1>(A.S, L.ids, L.nids, px, py, pz, G);
-            if (COUNT) tot_bytes += 16 * (unsigned long long)L.nids + 4 * (unsigned long long)G.n_nz;
-            if (G.den > kEpsWeight) {
-                const double v = G.num / G.den;
-                double c[4];
-                tf_eval(s_tf, A.M.tf_lo, A.M.tf_hi, v, c);
-                if (c[3] > 0.0) {
-                    const double alpha = 1.0 - pow(1.0 - c[3], sl / L.s1);
-                    if (GRAD != 0) {
-                        double g[3];
-                        if (GRAD == 1) {
-                            analytic_gradient(G, g);
-                        } else {
-                            int64_t ne = 0;
-                            central_gradient(A.S, A.M.grad_mode, px, py, pz, L.rid, L.ids, L.nids, v, g, &ne);
-                        }
-                        const double f = shade_factor(g, L.r);
-                        c[0] *= f; c[1] *= f; c[2] *= f;
-                    }
-                    const double wgt = alpha * (1.0 - L.acc[3]);
-                    L.acc[0] += wgt * c[0];
-                    L.acc[1] += wgt * c[1];
-                    L.acc[2] += wgt * c[2];
-                    L.acc[3] += wgt;
-                    if (L.acc[3] >= A.M.early) { last = true; early = true; }
-                }
-            }
-            if (last) in_region = false;
-        }
-        // ---- (4) walk toward the next region: KSTEPS node visits
-        if (has_ray && !early && nstate == kSearching) {
-#pragma unroll 1
-            for (int step = 0; step < KSTEPS; step++) {
-                KdNode n2 = nd;
-                uint8_t f2 = fl;
-                if (!(pre && step == 0) && L.w.node >= 0) {
-                    n2 = A.S.kd[L.w.node];
-                    f2 = A.vflags[L.w.node];
-                }
-                int rid = -1;
-                double ci = 0.0, co = 0.0;
-                const int st = kd_step(A.S, A.vflags, L.r, L.w, n2, f2, L.q_t, L.tmax, rid, ci, co);
-                if (st == 1) {
-                    nstate = kFound;
-                    L.nrid = rid;
-                    L.nci = ci;
-                    L.nco = co;
-                    break;
-                }
-                if (st == 2) {
-                    nstate = kExhausted;
-                    break;
-                }
-            }
-        }
-    }
-    // frame counters: one atomic per warp
-    for (int o = 16; o > 0; o >>= 1) {
-        tot_reg += __shfl_xor_sync(FULL, tot_reg, o);
-        tot_smp += __shfl_xor_sync(FULL, tot_smp, o);
-        tot_bytes += __shfl_xor_sync(FULL, tot_bytes, o);
-    }
-    if (lane == 0 && A.stats) {
-        atomicAdd(&A.stats[0], tot_reg);
-        atomicAdd(&A.stats[1], tot_smp);
-        if (COUNT) atomicAdd(&A.stats[2], tot_bytes);
-    }
-}
-
-// ---------------------------------------------------------------------------
 // k_warp: one warp per ray (default kernel).
 //
 // Traversal is a warp-cooperative *ordered frontier* over the region k-d tree:
@@ -362,21 +138,11 @@ constexpr int kWarpMinBlocks = 4;
 constexpr int kWarpsPerBlock = kWarpThreads / 32;
 constexpr int kWarpStack = 256;  // spilled frontier entries per warp
 constexpr int kRaysPerGrab = 8;  // rays taken per work-counter atomic
-// (sample, brick)-flattened chunk gather (march.cuh:gather_chunk).  The
-// per-sample brick loop runs max(nids) iterations per chunk, so about half of
-// its lane-brick slots idle (XB_DEBUG_CHUNKS: C3 5.1 bricks/sample vs 7.2 per
-// chunk, C2 2.4 vs 4.3, C5 1.6 vs 3.1), yet the flattened form — fewer rounds,
-// but partials through shared memory, a warp barrier per round and the
-// per-owner combine loop — measured slower every time: C2 12.3 vs 10.1 ms
-// (first pipeline), C3 1.21 vs 0.92 and C2 8.74 vs 6.31 (walk lists).  Kept
-// for A/B.
-constexpr bool kFlatGather = false;
-// k_warp work statistics (XB_DEBUG_CHUNKS at run time; compiled in only with
-// `make DEBUG_CHUNKS=1`: the counters cost k_warp registers)
-#ifndef XB_DEBUG_CHUNKS
-#define XB_DEBUG_CHUNKS 0
-#endif
-constexpr bool kDebugChunks = XB_DEBUG_CHUNKS != 0;
+// A (sample, brick)-flattened chunk gather (each lane one brick per round,
+// partials combined through shared memory) measured slower every time — C2
+// 12.3 vs 10.1 ms (first pipeline), C3 1.21 vs 0.92 and C2 8.74 vs 6.31 (walk
+// lists): the per-round barriers and the combine loop cost more than the idle
+// lane-brick slots of the per-sample loop.  Removed in round 2.
 
 struct SegQ {       // one visited region of the segment queue
     double ci, co;   // clipped interval
@@ -468,9 +234,6 @@ constexpr int kLeafCountMask = 0x0fffffff;
 constexpr int kLeafTruncated = 0x40000000;
 constexpr int kLeafHeavy = 0x20000000;  // > kShortSamples estimated samples (not for k_short)
 constexpr int kLeafTauStop = 0x10000000; // truncated by the opacity minorant (probably terminated)
-constexpr float kShortSamples = 24.f;  // defaults of RenderArgs.short_samples / short_leaves
-constexpr int kShortLeaves = 8;
-constexpr int kResume = 48;  // resume entries saved per truncated walk
 
 // pixel of a ray that meets no active region: transparent, or the iso colour
 __device__ __forceinline__ void write_empty_pixel(const RenderArgs& A, int64_t slot, int64_t out, bool clip_ok) {
@@ -828,39 +591,6 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk2(const __grid_constant__ 
     A.leaf_count[slot] = count | flags;
     (void)n_slots;
 }
-// Iso phase: one thread per iso-candidate ray runs _iso_ray (R/render.py:456-518)
-// over the regions k_walk listed for the iso active set, continuing with the
-// k-d walk from the root when the list was truncated (exact either way).
-template <bool COUNT>
-__global__ void __launch_bounds__(kWalkThreads) k_iso_march(const __grid_constant__ RenderArgs A, int64_t n_slots) {
-    const int64_t n_cand = (int64_t)A.walk_counter[1];
-    const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (ci >= n_cand) return;
-    const int64_t slot = A.long_list[ci];
-    const SlotPix sp = slot_pixel(A, slot);
-    Ray r;
-    pixel_ray(A, sp.x, sp.y, r);
-    const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
-    double tmin = 0.0, tmax = kTFar;
-    clip_ray(A.M, r, tmin, tmax);
-    const int lraw = A.leaf_count[slot];
-    const IsoList lst{A.leaves + slot * (int64_t)A.leaf_cap, lraw & kLeafCountMask, (lraw & kLeafTruncated) != 0};
-    RayStats st = {0, 0, 0};
-    double g[3], th = 0.0;
-    if (iso_ray<COUNT>(A.S, A.iflags, A.M, r, tmin, tmax, rho, th, g, st, nullptr, &lst)) {
-        A.iso_tend[slot] = th;
-        A.iso_shade[slot] = shade_factor(g, r);
-    }
-    if (COUNT && st.bytes) atomicAdd(&A.stats[2], (unsigned long long)st.bytes);
-    (void)n_slots;
-}
-
-// Iso phase, warp per ray: _iso_ray (R/render.py:456-518) evaluates f = value
-// - iso at t_in and at every lattice point of each iso-active region until the
-// sign changes; a region's lattice can hold thousands of points (its step is
-// half its finest cell width), so the warp evaluates 32 consecutive points at
-// once and takes the first sign change (ballot) — the same point the
-// sequential loop finds — then bisects 16 times and takes the analytic normal.
 template <bool COUNT>
 __global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const unsigned FULL = 0xffffffffu;
@@ -1127,8 +857,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     __shared__ SegQ s_q[kWarpsPerBlock][32];
     __shared__ RayAxes s_ray[kWarpsPerBlock];
     __shared__ RaySetup s_setup[kWarpsPerBlock][32];
-    extern __shared__ BrickPart s_part_dyn[];  // kFlatGather: 32 per warp (dynamic: static smem is at 42 KB)
-    BrickPart* s_part = s_part_dyn + (threadIdx.x >> 5) * 32;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
     __syncthreads();
     const unsigned FULL = 0xffffffffu;
@@ -1151,7 +879,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
         //      to [1, 32]): big grabs while the list is long, single rays at the end,
         //      where a fixed grab of 8 long rays left one warp working while the rest
         //      idled (tools/ab.py, ms, fixed 8 / guided: C3 1.20 / 0.95, C2 6.53 /
-        //      6.49, C5 3.63 / 3.62).  XB_GRAB_FIXED=N forces N rays per grab.
+        //      6.49, C5 3.63 / 3.62).
         //      With k_walk's leaf lists the work is its hit list (misses are done).
         unsigned long long b0 = 0;
         int grab = 32;
@@ -1309,9 +1037,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             }
                         }
                         FastAccum F;
-                        if (kFlatGather) {
-                            gather_chunk<GRAD == 1>(S, act, sq.ids, nids, px, py, pz, s_part, lane, F);
-                        } else if (act) {
+                        if (act) {
                             gather_shade<GRAD == 1>(S, (int64_t)sq.ids, nids, px, py, pz, F);
                         }
                         if (act) {
@@ -1766,18 +1492,6 @@ using RenderFn = void (*)(RenderArgs);
 using FrameFn = void (*)(RenderArgs, int64_t);
 
 template <int GRAD, bool ISO>
-static FrameFn frame_fn(bool count) {
-    return count ? (FrameFn)k_frame<GRAD, ISO, true> : (FrameFn)k_frame<GRAD, ISO, false>;
-}
-
-// tuning variants of the analytic, non-iso kernel (XB_KSTEPS / XB_MINB), for sweeps
-static FrameFn tuned_fn(int ksteps, int minb) {
-#define XB_T(K, B) if (ksteps == K && minb == B) return (FrameFn)k_frame<1, false, false, K, B>;
-    XB_T(2, 4) XB_T(3, 4) XB_T(4, 4) XB_T(5, 4) XB_T(6, 4) XB_T(8, 4)
-#undef XB_T
-    return nullptr;
-}
-template <int GRAD, bool ISO>
 static RenderFn tile_fn(bool count) {
     return count ? (RenderFn)k_render<GRAD, ISO, true> : (RenderFn)k_render<GRAD, ISO, false>;
 }
@@ -1787,16 +1501,6 @@ static int grad_index(int mode) { return mode == 0 ? 0 : (mode == 1 ? 1 : 2); }
 template <int GRAD, bool ISO>
 static FrameFn warp_fn(bool count) {
     return count ? (FrameFn)k_warp<GRAD, ISO, true> : (FrameFn)k_warp<GRAD, ISO, false>;
-}
-
-// XB_KERNEL=frame | tile selects the per-lane kernels for A/B measurements
-static int kernel_choice() {
-    const char* tr = getenv("XB_TRAVERSAL");
-    if (tr && strcmp(tr, "lbvh") == 0) return 2;  // per-visit LBVH queries run in the one-thread-per-pixel kernel
-    const char* e = getenv("XB_KERNEL");
-    if (e && strcmp(e, "tile") == 0) return 2;
-    if (e && strcmp(e, "frame") == 0) return 1;
-    return 0;
 }
 
 // slots i in [0, n) with pred(i), in order -> out, count -> *n_out (device)
@@ -1826,7 +1530,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
     const bool iso = A.M.iso_on != 0;
     const int g = grad_index(A.M.grad_mode);
     const int64_t n_slots = n_tiles_local * kTileW * kTileH;
-    if (iso && (!A.leaves || kernel_choice() != 0)) {  // per-lane iso pass (frame / tile / LBVH paths)
+    if (iso && (!A.leaves || A.kernel != 0)) {  // per-lane iso pass (tile / LBVH / frontier-only paths)
         void* args[] = {(void*)&A, (void*)&n_slots};
         const void* fn = count ? (const void*)k_iso_pass<true> : (const void*)k_iso_pass<false>;
         XB_CUDA(cudaLaunchKernel(fn, dim3(grid_for(n_slots, 128)), dim3(128), args, 0, s));
@@ -1849,10 +1553,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
                                  0, s));
         XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads * kRouteSub)),
                                  dim3(kWalkThreads), iargs, 0, s));
-        if (getenv("XB_ISO_LANE")) {  // A/B: one thread per iso ray
-            const void* mf = count ? (const void*)k_iso_march<true> : (const void*)k_iso_march<false>;
-            XB_CUDA(cudaLaunchKernel(mf, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads), iargs, 0, s));
-        } else {
+        {
             const void* mf = count ? (const void*)k_iso_warp<true> : (const void*)k_iso_warp<false>;
             int dev = 0, sms = 0, per_sm = 0;
             XB_CUDA(cudaGetDevice(&dev));
@@ -1865,13 +1566,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         }
         XB_CUDA(cudaMemsetAsync(A.walk_counter, 0, 5 * sizeof(unsigned long long), s));  // volume phase lists
     }
-    const int kc = A.M.use_tree ? 2 : kernel_choice();  // cell location: the one-thread-per-pixel kernel
-    {  // k_warp guided ray-grab schedule (tuning knob XB_GRAB_DIV)
-        RenderArgs& W = const_cast<RenderArgs&>(A);
-        W.grab_div = getenv("XB_GRAB_DIV") ? std::max(1, atoi(getenv("XB_GRAB_DIV"))) : 4;
-        W.grab_fixed = getenv("XB_GRAB_FIXED") ? std::min(32, atoi(getenv("XB_GRAB_FIXED"))) : 0;
-    }
-    if (kc == 2) {
+    if (A.kernel == 1) {  // one thread per pixel: LBVH traversal, cell location, tuning.kernel = 1
         RenderFn fn;
         if (g == 0) fn = iso ? tile_fn<0, true>(count) : tile_fn<0, false>(count);
         else if (g == 1) fn = iso ? tile_fn<1, true>(count) : tile_fn<1, false>(count);
@@ -1881,19 +1576,8 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         return;
     }
     FrameFn fn;
-    int threads;
-    if (kc == 1) {
-        threads = kFrameThreads;
-        if (g == 0) fn = iso ? frame_fn<0, true>(count) : frame_fn<0, false>(count);
-        else if (g == 1) fn = iso ? frame_fn<1, true>(count) : frame_fn<1, false>(count);
-        else fn = iso ? frame_fn<2, true>(count) : frame_fn<2, false>(count);
-        if (g == 1 && !iso && !count && (getenv("XB_KSTEPS") || getenv("XB_MINB"))) {
-            const int ks = getenv("XB_KSTEPS") ? atoi(getenv("XB_KSTEPS")) : kKdSteps;
-            const int mb = getenv("XB_MINB") ? atoi(getenv("XB_MINB")) : 4;
-            if (FrameFn t = tuned_fn(ks, mb)) fn = t;
-        }
-    } else {
-        threads = kWarpThreads;
+    const int threads = kWarpThreads;
+    {
         if (A.leaves) {
             RenderArgs& W = const_cast<RenderArgs&>(A);
             const double e = std::min(A.M.early, 0.999999);
@@ -1901,9 +1585,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             // did not terminate there resumes in k_warp, so the margin only trades walk length
             // against resumes (tools/ab.py, ms, margin 2 / 1 / 0 / -1: C5 3.48 / 3.38 / 3.31 / 3.57,
             // C2 6.30 / 6.30 / 6.27 / 6.42, C3 flat)
-            const double margin = getenv("XB_TAU_MARGIN") ? atof(getenv("XB_TAU_MARGIN")) : 0.0;
-            W.walk_tau_stop = (float)(-std::log(1.0 - e) + margin);
-            if (getenv("XB_WALK_NOTAU")) W.walk_tau_stop = INFINITY;
+            W.walk_tau_stop = (float)(-std::log(1.0 - e));
             void* wargs[] = {(void*)&A, (void*)&n_slots};
             XB_CUDA(cudaLaunchKernel((const void*)k_classify, dim3(grid_for(n_slots, kWalkThreads)),
                                      dim3(kWalkThreads), wargs, 0, s));
@@ -1935,24 +1617,13 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         if (g == 0) fn = iso ? warp_fn<0, true>(count) : warp_fn<0, false>(count);
         else if (g == 1) fn = iso ? warp_fn<1, true>(count) : warp_fn<1, false>(count);
         else fn = iso ? warp_fn<2, true>(count) : warp_fn<2, false>(count);
-        if (g == 1 && !iso && !count && getenv("XB_WMINB")) {  // occupancy sweep (tools/ab.py)
-            const int mb = atoi(getenv("XB_WMINB"));
-            if (mb == 2) fn = (FrameFn)k_warp<1, false, false, 2>;
-            if (mb == 3) fn = (FrameFn)k_warp<1, false, false, 3>;
-            if (mb == 5) fn = (FrameFn)k_warp<1, false, false, 5>;
-        }
     }
     int dev = 0, sms = 0, per_sm = 0;
     XB_CUDA(cudaGetDevice(&dev));
     XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     size_t dyn = 0;
-    if (kc == 0 && kFlatGather) {
-        dyn = kWarpsPerBlock * 32 * sizeof(BrickPart);
-        XB_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
-    }
     XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, dyn));
-    const int64_t per_thread = kc == 1 ? 1 : 32;  // k_warp: one ray per warp at a time
-    const int64_t want = (n_slots * per_thread + threads - 1) / threads;
+    const int64_t want = (n_slots * 32 + threads - 1) / threads;  // k_warp: one ray per warp at a time
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), want));
     void* args[] = {(void*)&A, (void*)&n_slots};
     XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(threads), args, dyn, s));

@@ -5,13 +5,18 @@
 namespace xb {
 
 constexpr int kTileW = 16, kTileH = 8;  // screen tile; a warp owns an 8x4 quarter
-constexpr int kFrameThreads = 128;      // persistent k_frame block size
-constexpr int kKdSteps = 5;             // k-d node visits per k_frame iteration (tools/sweep.py)
-constexpr int kFrameMinBlocks = 4;      // 128 regs/thread -> 16 warps/SM (more spills, fewer hurt)
 
 // Passed by value as a __grid_constant__ kernel parameter (~8.6 KB < 32 KB):
 // the call needs no device allocation, so concurrent renders are reentrant.
 constexpr int kWalkThreads = 128;  // k_classify / k_walk / k_route / k_short block size
+constexpr float kShortSamples = 24.f;  // short ray: complete list of <= kShortLeaves leaves, <= kShortSamples
+constexpr int kShortLeaves = 8;        // estimated samples (RenderArgs.short_samples / short_leaves)
+constexpr int kResume = 48;            // resume entries saved per truncated walk
+// k_warp work statistics, compiled in only with `make DEBUG_CHUNKS=1` (the counters cost k_warp registers)
+#ifndef XB_DEBUG_CHUNKS
+#define XB_DEBUG_CHUNKS 0
+#endif
+constexpr bool kDebugChunks = XB_DEBUG_CHUNKS != 0;
 
 struct RenderArgs {
     SceneView S;
@@ -57,7 +62,8 @@ struct RenderArgs {
     int short_leaves;                  // short ray: complete list of <= short_leaves leaves ...
     float short_samples;               // ... and <= short_samples estimated samples
     float walk_tau_stop;               // k_walk stops listing once the opacity minorant passes this depth
-    int use_lbvh;                      // XB_TRAVERSAL=lbvh: per-visit LBVH closest-hit queries (tile kernel)
+    int use_lbvh;                      // tuning.traversal = 1: per-visit LBVH closest-hit queries (k_render)
+    int kernel;                        // 0: walk pipeline + k_warp; 1: one thread per pixel (k_render)
     LbvhView vlb, ilb;                 // LBVHs of the volume / iso active sets
     double* iso_tend;           // per slot: volume t_end (iso hit or clip end)
     double* iso_shade;          // per slot: headlight factor of the iso hit, < 0 when none

@@ -246,36 +246,28 @@ def _params(meta):
                        seed=meta["seed"], gradient_mode=meta["gradient_mode"], clip_planes=planes)
 
 
-KERNEL_ENVS = {
-    "warp": {},                        # default: k_classify + k_walk leaf lists + k_warp
-    "warp_cap1": {"XB_LEAF_CAP": "1"},  # every long ray falls back to the warp frontier
-    "warp_nowalk": {"XB_WALK": "0"},   # k_warp's frontier only
-    "warp_short": {"XB_SHORT": "1"},   # short rays one per lane (k_warp's second phase) even when few
-    "warp_kshort": {"XB_SHORT": "1", "XB_FUSE_SHORT": "0"},  # ... through the separate k_short launch
-    "warp_2pass": {"XB_WALK_CAP1": "2", "XB_WALK2_MIN": "0"},  # k_walk2 continues (nearly) every walk
-    "frame": {"XB_KERNEL": "frame"},   # per-lane persistent kernel
-    "tile": {"XB_KERNEL": "tile"},     # one thread per pixel
-    "lbvh": {"XB_TRAVERSAL": "lbvh"},  # per-visit LBVH closest-hit queries (the reference's traversal)
+KERNEL_VARIANTS = {  # xb_tuning fields (include/exabricks.h) of each frame-pipeline variant
+    "warp": {},                                  # default: k_classify + k_walk leaf lists + k_warp
+    "warp_cap1": {"leaf_cap": 1},                # every long ray falls back to the warp frontier
+    "warp_nowalk": {"walk_lists": 0},            # k_warp's frontier only
+    "warp_short": {"short_rays": 1},             # short rays one per lane (k_warp's second phase) even when few
+    "warp_kshort": {"short_rays": 1, "fuse_short": 0},  # ... through the separate k_short launch
+    "warp_2pass": {"walk_cap1": 2, "walk2_min": 0},     # k_walk2 continues (nearly) every walk
+    "tile": {"kernel": 1},                       # one thread per pixel
+    "lbvh": {"traversal": 1},                    # per-visit LBVH closest-hit queries (the reference's traversal)
 }
-_ENV_KEYS = ("XB_KERNEL", "XB_LEAF_CAP", "XB_WALK", "XB_TRAVERSAL", "XB_SHORT", "XB_WALK_CAP1", "XB_WALK2_MIN",
-             "XB_FUSE_SHORT")
 
 
 @pytest.fixture
 def kernel_env(request):
-    """Select the march-kernel variant through its environment switches."""
-    import os
+    """Select the frame-pipeline variant (xb_tuning_set) for the test."""
+    from paper_2009_03076_b200 import _native as N
 
-    old = {k: os.environ.pop(k, None) for k in _ENV_KEYS}
-    os.environ.update(KERNEL_ENVS[request.param])
-    yield request.param
-    for k in _ENV_KEYS:
-        os.environ.pop(k, None)
-        if old[k] is not None:
-            os.environ[k] = old[k]
+    with N.tuning(**KERNEL_VARIANTS[request.param]):
+        yield request.param
 
 
-@pytest.mark.parametrize("kernel_env", sorted(KERNEL_ENVS), indirect=True)
+@pytest.mark.parametrize("kernel_env", sorted(KERNEL_VARIANTS), indirect=True)
 @pytest.mark.parametrize("key", _frame_keys())
 def test_frames_match_reference(xb, key, frames, kernel_env):
     from paper_2009_03076_b200.accel import TransferFunction
@@ -472,15 +464,11 @@ def test_acceptance_million_cells_vs_oracle(xb):
     # whole frame: the warp-per-ray kernel (default) must equal the per-lane
     # persistent kernel and the one-thread-per-pixel kernel everywhere, on every
     # repetition
-    import os
+    from paper_2009_03076_b200 import _native as N
 
-    for kern in ("tile", "frame", "warp_cap1", "warp_nowalk", "warp_short", "warp_kshort", "warp_2pass", "lbvh"):
-        os.environ.update(KERNEL_ENVS[kern])
-        try:
+    for kern in ("tile", "warp_cap1", "warp_nowalk", "warp_short", "warp_kshort", "warp_2pass", "lbvh"):
+        with N.tuning(**KERNEL_VARIANTS[kern]):
             u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)
-        finally:
-            for k in _ENV_KEYS:
-                os.environ.pop(k, None)
         assert np.array_equal(cnt, cntt), kern
         assert np.abs(f64 - f64t).max() <= RGBA_TOL, kern
     for _ in range(3):

@@ -50,12 +50,13 @@ def test_struct_sizes_match_c_compiler(tmp_path):
     from paper_2009_03076_b200 import _native as N
 
     src = tmp_path / "sz.c"
-    src.write_text('#include <stdio.h>\n#include "exabricks.h"\nint main(void){printf("%zu %zu %zu\\n",'
-                   'sizeof(xb_camera), sizeof(xb_march), sizeof(xb_synth_spec));return 0;}\n')
+    src.write_text('#include <stdio.h>\n#include "exabricks.h"\nint main(void){printf("%zu %zu %zu %zu\\n",'
+                   'sizeof(xb_camera), sizeof(xb_march), sizeof(xb_synth_spec), sizeof(xb_tuning));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
-    assert got == [ctypes.sizeof(N.XbCamera), ctypes.sizeof(N.XbMarch), ctypes.sizeof(N.XbSynthSpec)]
+    assert got == [ctypes.sizeof(N.XbCamera), ctypes.sizeof(N.XbMarch), ctypes.sizeof(N.XbSynthSpec),
+                   ctypes.sizeof(N.XbTuning)]
 
 
 def test_compute_fails_loudly_without_device():

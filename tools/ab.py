@@ -1,5 +1,9 @@
-"""A/B frame timing of march-kernel variants (XB_KERNEL values), interleaved:
-python tools/ab.py CONFIG warp,frame [reps]"""
+"""A/B frame timing of frame-pipeline variants (xb_tuning fields), interleaved:
+python tools/ab.py CONFIG warp,tile,lbvh,k:leaf_cap=48+short_rays=0 [reps]
+
+warp = the defaults; tile = one thread per pixel; lbvh = per-visit LBVH
+queries (the reference's traversal); k:F=V+F2=V2 sets xb_tuning fields.
+Other libraries: XB_LIB=path/to/libexabricks.so."""
 import os
 import sys
 
@@ -21,60 +25,25 @@ regions = build_regions(model)
 tf = bench.tf_for(model.value_range(0), cfg)
 scene = build_scene(model, regions, tf, iso_value=cfg.get("iso"))
 cam = bench.camera_for(regions.bounds, cfg, 0)
-params = MarchParams(seed=0, gradient_mode=cfg["gradient"])
-W, H = cfg["res"]
-out = torch.empty((H, W, 4), dtype=torch.uint8, device="cuda")
-flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-stream = torch.cuda.current_stream()
+params = MarchParaNAMED = {"warp": {}, "tile": {"kernel": 1}, "lbvh": {"traversal": 1}, "nowalk": {"walk_lists": 0},
+         "short": {"short_rays": 1}, "noshort": {"short_rays": 0}, "kshort": {"short_rays": 1, "fuse_short": 0}}
+
+
+def fields_of(v):
+    if v.startswith("k:"):
+        return {kv.split("=")[0]: int(kv.split("=")[1]) for kv in v[2:].split("+")}
+    return NAMED[v]
 
 
 def setv(v):
-    for k in [k for k in os.environ if k.startswith("XB_") and k != "XB_LIB"]:
-        os.environ.pop(k)
-    """warp | frame | tile | warpN (k_warp with __launch_bounds__ min blocks N) | gD (guided grab divisor D)"""
-    for k in ("XB_KERNEL", "XB_WMINB", "XB_GRAB_DIV", "XB_GRAB_FIXED", "XB_WALK", "XB_LEAF_CAP", "XB_WALK_NOTAU",
-              "XB_TRAVERSAL", "XB_SHORT", "XB_SHORT_LEAVES", "XB_SHORT_SAMPLES"):
-        os.environ.pop(k, None)
-    for k in ("XB_WALK_CAP1", "XB_WALK2_MIN", "XB_WALK_CAP2", "XB_CUT_TAU"):
-        os.environ.pop(k, None)
-    if v.startswith("e:"):  # e:K=V+K2=V2: arbitrary XB_* settings
-        for kv in v[2:].split("+"):
-            k, val = kv.split("=")
-            os.environ[k] = val
-        return
-    if v.startswith("w2_"):  # w2_X_Y: pass-1 cap X, pass-2 cap Y
-        os.environ["XB_WALK_CAP1"], os.environ["XB_WALK_CAP2"] = v[3:].split("_")
-        return
-    if v.startswith("c1_") :  # c1_X_Y: pass-1 cap X, pass-2 minimum Y
-        os.environ["XB_WALK_CAP1"], os.environ["XB_WALK2_MIN"] = v[3:].split("_")
-        return
-    if v.startswith("sl") and "_" in v:  # slL_S: short-ray thresholds
-        os.environ["XB_SHORT_LEAVES"], os.environ["XB_SHORT_SAMPLES"] = v[2:].split("_")
-        return
-    if v == "cutnotau":
-        os.environ["XB_CUT_TAU"] = "0"
-        return
-    if v == "short":
-        os.environ["XB_SHORT"] = "1"
-    elif v == "noshort":
-        os.environ["XB_SHORT"] = "0"
-    elif v == "lbvh":
-        os.environ["XB_TRAVERSAL"] = "lbvh"
-    elif v == "notau":
-        os.environ["XB_WALK_NOTAU"] = "1"
-    elif v == "nowalk":
-        os.environ["XB_WALK"] = "0"
-    elif v.startswith("cap") and v[3:].isdigit():
-        os.environ["XB_LEAF_CAP"] = v[3:]
-    elif v.startswith("f") and v[1:].isdigit():
-        os.environ["XB_GRAB_FIXED"] = v[1:]
-    elif v.startswith("g") and v[1:].isdigit():  # guided grabs with divisor D
-        os.environ["XB_GRAB_DIV"] = v[1:]
-        os.environ["XB_GRAB_FIXED"] = "0"
-    elif v.startswith("warp") and len(v) > 4:
-        os.environ["XB_WMINB"] = v[4:]
-    elif v != "warp":
-        os.environ["XB_KERNEL"] = v
+    from paper_2009_03076_b200 import _native as N
+    import ctypes as C
+
+    t = N.XbTuning()
+    N.lib().xb_tuning_defaults(C.byref(t))
+    for k, val in fields_of(v).items():
+        setattr(t, k, val)
+    N.check(N.lib().xb_tuning_set(C.byref(t)))
 
 
 times = {v: [] for v in variants}

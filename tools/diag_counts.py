@@ -26,8 +26,10 @@ u8, f64, cnt, st = render_frame_float(scene, cam, tf, params, count_bytes=True)
 print("count variant", st, cnt[..., 1].sum(), cnt[..., 0].sum())
 u8b, f64b, cntb, stb = render_frame_float(scene, cam, tf, params)
 print("float variant", stb, cntb[..., 1].sum())
-os.environ["XB_KERNEL"] = "tile"
-u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)
+from paper_2009_03076_b200 import _native as N  # noqa: E402
+
+with N.tuning(kernel=1):
+    u8t, f64t, cntt, stt = render_frame_float(scene, cam, tf, params)
 print("tile kernel", stt, cntt[..., 1].sum())
 d = np.abs(f64 - f64t).max()
 print("max |f64 frame - tile|", d, "count mismatches", int((cnt != cntt).any(-1).sum()))
