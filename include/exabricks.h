@@ -145,8 +145,10 @@ typedef struct {
  * world == 1 it is the (H, W, 4) image, otherwise the rank's packed tiles
  * (xb_tile_count() tiles x 128 px x 4 B).  rgba_f64 / px_counts (int32
  * regions, samples per pixel): optional parity outputs, same layout, host or
- * device.  stats (host, may be NULL): [regions, samples, algorithmic bytes]
- * (bytes only when count_bytes != 0).  `vol` may not be NULL; `iso` may. */
+ * device.  stats (may be NULL): [regions, samples, algorithmic bytes] (bytes
+ * only when count_bytes != 0); a host pointer makes the call synchronous, a
+ * device pointer (3 x int64) is filled on `stream` without host sync.  `vol`
+ * may not be NULL; `iso` may. */
 int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_active* vol, const xb_active* iso,
               const xb_camera* cam, const xb_march* mp, int32_t tile_rank, int32_t tile_world, void* rgba8,
               double* rgba_f64, int32_t* px_counts, int64_t* stats, int32_t count_bytes, void* stream);
@@ -165,11 +167,16 @@ typedef struct {
     int32_t short_rays; /* -1 (default): lane-per-ray phase when >= 1000 x SMs short rays; 0: never; 1: always */
     int64_t walk2_min;  /* k_walk2 runs when >= walk2_min walks were cut; -1 (default): 500 x SMs */
     int32_t fuse_short; /* 1 (default): short rays run inside k_warp after the long ones; 0: separate k_short */
-    int32_t reserved;
+    int32_t time_march; /* 1: record a CUDA event pair around every k_warp launch (xb_march_times); default 0 */
 } xb_tuning;
 void xb_tuning_defaults(xb_tuning* t);
 int xb_tuning_get(xb_tuning* t);
 int xb_tuning_set(const xb_tuning* t); /* NULL restores the defaults */
+/* Device time of the march kernel (k_warp, the frame's dominant kernel) of the
+ * frames rendered with tuning.time_march = 1: waits for the recorded events and
+ * returns up to `cap` elapsed times in ms, oldest first, in ms[0 .. *n); the
+ * returned records are forgotten. */
+int xb_march_times(double* ms, int32_t cap, int32_t* n);
 
 int xb_tile_count(int32_t width, int32_t height, int32_t rank, int32_t world, int64_t* n_tiles, int32_t* tile_px);
 /* gathered packed tiles (rank-major, tiles_per_rank each) -> (H, W, 4) image; device pointers */

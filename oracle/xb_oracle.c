@@ -196,14 +196,59 @@ static int cell_cmp(const void* a, const void* b) {
     return x < y ? -1 : (x > y); /* lexsort is stable */
 }
 
+/* The same stable lexsort as an LSD radix sort on packed (level, k, j, i)
+ * keys (offset by their minima) when they fit in 64 bits: equal keys keep
+ * their input order, like np.lexsort.  Returns 0 when they do not fit. */
+static int bits_for(int64_t range) { int b = 0; while (b < 63 && ((int64_t)1 << b) <= range) b++; return b; }
+static int radix_lexsort(int64_t n, const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* lev,
+                         int64_t* order) {
+    if (n < 2) return 1;
+    int64_t mn[4], mx[4];
+    const int32_t* a[4] = {i, j, k, lev};
+    for (int c = 0; c < 4; c++) {
+        mn[c] = INT64_MAX; mx[c] = INT64_MIN;
+        for (int64_t t = 0; t < n; t++) { if (a[c][t] < mn[c]) mn[c] = a[c][t]; if (a[c][t] > mx[c]) mx[c] = a[c][t]; }
+    }
+    int b[4], tot = 0;
+    for (int c = 0; c < 4; c++) { b[c] = bits_for(mx[c] - mn[c]); tot += b[c]; }
+    if (tot > 64) return 0;
+    uint64_t* key = malloc(sizeof(uint64_t) * n);
+    uint64_t* key2 = malloc(sizeof(uint64_t) * n);
+    int64_t* ord2 = malloc(sizeof(int64_t) * n);
+    for (int64_t t = 0; t < n; t++) {  /* i lowest, level highest */
+        uint64_t v = 0; int sh = 0;
+        for (int c = 0; c < 4; c++) { v |= (uint64_t)(a[c][t] - mn[c]) << sh; sh += b[c]; }
+        key[t] = v;
+    }
+    int64_t cnt[65536];
+    for (int pass = 0; pass * 16 < tot; pass++) {
+        int sh = pass * 16;
+        memset(cnt, 0, sizeof cnt);
+        for (int64_t t = 0; t < n; t++) cnt[(key[t] >> sh) & 0xffff]++;
+        int64_t sum = 0;
+        for (int d = 0; d < 65536; d++) { int64_t c = cnt[d]; cnt[d] = sum; sum += c; }
+        for (int64_t t = 0; t < n; t++) {
+            int64_t p = cnt[(key[t] >> sh) & 0xffff]++;
+            key2[p] = key[t];
+            ord2[p] = order[t];
+        }
+        uint64_t* tk = key; key = key2; key2 = tk;
+        memcpy(order, ord2, sizeof(int64_t) * n);
+    }
+    free(key); free(key2); free(ord2);
+    return 1;
+}
+
 XO_API xo_bricks_t* xo_build_bricks(int64_t n, const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* lev,
                                     const float* vals, int64_t F, int64_t maxw, int keep_tree) {
     xo_bricks_t* out = calloc(1, sizeof(xo_bricks_t));
     out->n_fields = F;
     int64_t* order = malloc(sizeof(int64_t) * (n ? n : 1));
     for (int64_t t = 0; t < n; t++) order[t] = t;
-    srt_i = i; srt_j = j; srt_k = k; srt_l = lev;
-    qsort(order, (size_t)n, sizeof(int64_t), cell_cmp);
+    if (!radix_lexsort(n, i, j, k, lev, order)) {
+        srt_i = i; srt_j = j; srt_k = k; srt_l = lev;
+        qsort(order, (size_t)n, sizeof(int64_t), cell_cmp);
+    }
     int64_t *ci = malloc(8 * (n + 1)), *cj = malloc(8 * (n + 1)), *ck = malloc(8 * (n + 1)), *cl = malloc(8 * (n + 1));
     float* cv = malloc(sizeof(float) * (n * F + 1));
     for (int64_t t = 0; t < n; t++) {

@@ -57,7 +57,7 @@ class XbTuning(C.Structure):
     """xb_tuning (include/exabricks.h): frame-pipeline variants for A/B runs and the parity matrix."""
 
     _fields_ = [("kernel", i32), ("traversal", i32), ("walk_lists", i32), ("leaf_cap", i32), ("walk_cap1", i32),
-                ("short_rays", i32), ("walk2_min", i64), ("fuse_short", i32), ("reserved", i32)]
+                ("short_rays", i32), ("walk2_min", i64), ("fuse_short", i32), ("time_march", i32)]
 
 
 # exported symbol -> (restype, argtypes); tests check every declared symbol
@@ -93,6 +93,7 @@ SIGNATURES = {
     "xb_tuning_defaults": (None, [P]),
     "xb_tuning_get": (C.c_int, [P]),
     "xb_tuning_set": (C.c_int, [P]),
+    "xb_march_times": (C.c_int, [P, i32, P]),
     "xb_tile_count": (C.c_int, [i32, i32, i32, i32, P, P]),
     "xb_unpack_tiles": (C.c_int, [P, i64, i32, i32, i32, P, P]),
     "xb_integrate_rays": (C.c_int, [P, P, i32, P, P, i64, P, P, P, P, P, P, P]),

@@ -562,7 +562,39 @@ xb_tuning tuning_snapshot() {
     std::lock_guard<std::mutex> g(g_tuning_mu);
     return g_tuning;
 }
+
+// k_warp event pairs of frames rendered with tuning.time_march (xb_march_times)
+struct MarchEvents {
+    int device;
+    cudaEvent_t ev[2];
+};
+std::mutex g_events_mu;
+std::vector<MarchEvents> g_events;
 }  // namespace
+
+int xb_march_times(double* ms, int32_t cap, int32_t* n) {
+    return guarded([&] {
+        XB_CHECK(n && (ms || cap == 0) && cap >= 0, XB_ERR_ARG, "bad march-times arguments");
+        std::vector<MarchEvents> take;
+        {
+            std::lock_guard<std::mutex> g(g_events_mu);
+            const size_t k = std::min<size_t>(g_events.size(), (size_t)cap);
+            take.assign(g_events.begin(), g_events.begin() + k);
+            g_events.erase(g_events.begin(), g_events.begin() + k);
+        }
+        int32_t got = 0;
+        for (auto& e : take) {
+            xb::DeviceGuard dg(e.device);
+            float t = 0.f;
+            XB_CUDA(cudaEventSynchronize(e.ev[1]));
+            XB_CUDA(cudaEventElapsedTime(&t, e.ev[0], e.ev[1]));
+            ms[got++] = (double)t;
+            cudaEventDestroy(e.ev[0]);
+            cudaEventDestroy(e.ev[1]);
+        }
+        *n = got;
+    });
+}
 
 void xb_tuning_defaults(xb_tuning* t) {
     if (!t) return;
@@ -575,6 +607,7 @@ void xb_tuning_defaults(xb_tuning* t) {
     t->short_rays = -1;
     t->walk2_min = -1;
     t->fuse_short = 1;
+    t->time_march = 0;
 }
 
 int xb_tuning_get(xb_tuning* t) {
@@ -741,7 +774,18 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             A->leaves = leaf_buf + (3 + res_words) * ns1;
             A->leaf_cap = cap;
         }
+        MarchEvents me{m->m.device, {nullptr, nullptr}};
+        A->march_events = nullptr;
+        if (T.time_march && A->kernel == 0) {
+            XB_CUDA(cudaEventCreate(&me.ev[0]));
+            XB_CUDA(cudaEventCreate(&me.ev[1]));
+            A->march_events = me.ev;
+        }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
+        if (A->march_events) {
+            std::lock_guard<std::mutex> eg(g_events_mu);
+            g_events.push_back(me);
+        }
         if (A->dbg) {
             unsigned long long d[7];
             XB_CUDA(cudaMemcpyAsync(d, A->dbg, sizeof d, cudaMemcpyDeviceToHost, s));
@@ -757,11 +801,13 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         of.finish();
         oc.finish();
         unsigned long long hs[3] = {0, 0, 0};
-        if (dstats) XB_CUDA(cudaMemcpyAsync(hs, dstats, sizeof hs, cudaMemcpyDeviceToHost, s));
+        const bool dev_stats = stats && is_device_ptr(stats);  // device counters: no host synchronisation
+        if (dev_stats) XB_CUDA(cudaMemcpyAsync(stats, dstats, sizeof hs, cudaMemcpyDeviceToDevice, s));
+        else if (dstats) XB_CUDA(cudaMemcpyAsync(hs, dstats, sizeof hs, cudaMemcpyDeviceToHost, s));
         XB_CUDA(cudaFreeAsync(scratch, s));
-        const bool host_out = o8.owned || of.owned || oc.owned || dstats;
+        const bool host_out = o8.owned || of.owned || oc.owned || (dstats && !dev_stats);
         if (host_out) XB_CUDA(cudaStreamSynchronize(s));
-        if (stats) {
+        if (stats && !dev_stats) {
             stats[0] = (int64_t)hs[0];
             stats[1] = (int64_t)hs[1];
             stats[2] = (int64_t)hs[2];

@@ -1626,7 +1626,10 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
     const int64_t want = (n_slots * 32 + threads - 1) / threads;  // k_warp: one ray per warp at a time
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), want));
     void* args[] = {(void*)&A, (void*)&n_slots};
+    cudaEvent_t* ev = (cudaEvent_t*)A.march_events;
+    if (ev) XB_CUDA(cudaEventRecord(ev[0], s));
     XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(threads), args, dyn, s));
+    if (ev) XB_CUDA(cudaEventRecord(ev[1], s));
 }
 
 // ---------------------------------------------------------------------------

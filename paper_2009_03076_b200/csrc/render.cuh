@@ -64,6 +64,7 @@ struct RenderArgs {
     float walk_tau_stop;               // k_walk stops listing once the opacity minorant passes this depth
     int use_lbvh;                      // tuning.traversal = 1: per-visit LBVH closest-hit queries (k_render)
     int kernel;                        // 0: walk pipeline + k_warp; 1: one thread per pixel (k_render)
+    void* march_events;                // cudaEvent_t[2] recorded around the k_warp launch, or NULL
     LbvhView vlb, ilb;                 // LBVHs of the volume / iso active sets
     double* iso_tend;           // per slot: volume t_end (iso hit or clip end)
     double* iso_shade;          // per slot: headlight factor of the iso hit, < 0 when none

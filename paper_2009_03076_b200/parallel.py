@@ -72,41 +72,88 @@ def unpack_host(packed_by_rank, width: int, height: int, world: int):
 
 
 class TiledRenderer:
-    """Render one frame across all ranks of the default process group."""
+    """Render one frame across all ranks of the default process group.
 
-    def __init__(self, scene, width: int, height: int, device=None):
+    Each rank renders its tiles into `packed` (global pixel index into the
+    jitter hash), `exchange()` all-gathers the packed tiles (NCCL on B200,
+    gloo in the CPU tests), `assemble()` scatters them into the image on rank
+    0 (`xb_unpack_tiles` on the device; `unpack_host` mirrors it), and with
+    `stats=True` the frame counters [regions, samples] are all-reduced — the
+    multi-GPU `FrameStats` (R/render.py:684-691)."""
+
+    def __init__(self, scene, width: int, height: int, device=None, group=None):
         import torch
         import torch.distributed as dist
 
         self.torch, self.dist = torch, dist
+        self.group = group
         self.scene = scene
-        self.world = dist.get_world_size() if dist.is_initialized() else 1
-        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.width, self.height = width, height
-        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
         self.slots = tiles_per_rank(width, height, self.world)
         self.n_local = tiles_of_rank(width, height, self.rank, self.world)
         self.packed = torch.zeros((self.slots * TILE_PX, 4), dtype=torch.uint8, device=self.device)
         self.gathered = torch.empty((self.world * self.slots * TILE_PX, 4), dtype=torch.uint8, device=self.device)
         self.image = torch.empty((height, width, 4), dtype=torch.uint8, device=self.device)
+        self.counters = torch.zeros(3, dtype=torch.int64, device=self.device)
 
-    def render(self, camera, tf, params, gather=True):
+    def _check_camera(self, camera):
+        # xb_render sizes its output from the camera: a mismatch would write past
+        # (or leave holes in) the buffers allocated for width x height here
+        if camera.width != self.width or camera.height != self.height:
+            raise ValueError(f"camera is {camera.width}x{camera.height} but the renderer was built for "
+                             f"{self.width}x{self.height}")
+
+    def exchange(self):
+        """All-gather every rank's packed tiles into `gathered` (rank-major)."""
+        if self.world > 1:
+            self.dist.all_gather_into_tensor(self.gathered, self.packed, group=self.group)
+        return self.gathered
+
+    def reduce_counters(self):
+        """Sum [regions, samples, bytes] over the ranks (one all-reduce)."""
+        if self.world > 1:
+            self.dist.all_reduce(self.counters, group=self.group)
+        return self.counters
+
+    def assemble(self, stream=None):
+        """Rank 0: scatter the gathered tiles into `image` on the device."""
+        if self.rank != 0:
+            return None
+        if stream is None:
+            stream = self.torch.cuda.current_stream().cuda_stream
+        N.check(N.lib().xb_unpack_tiles(N.ptr(self.gathered.data_ptr()), self.slots, self.world, self.width,
+                                        self.height, N.ptr(self.image.data_ptr()), N.ptr(stream)))
+        return self.image
+
+    def render(self, camera, tf, params, gather=True, stats=False):
         """Render this rank's tiles; with `gather`, assemble the image on rank 0
-        (returned device tensor on rank 0, None elsewhere)."""
+        (device tensor on rank 0, None elsewhere).  With `stats`, returns
+        (image, counters) where counters = [regions, samples, 0] summed over the
+        ranks (int64 device tensor, every rank)."""
         from .render import render_native
 
+        self._check_camera(camera)
         stream = self.torch.cuda.current_stream().cuda_stream
+        dev_stats = self.counters.data_ptr() if stats else None
         if self.world == 1:
-            render_native(self.scene, camera, tf, params, self.image.data_ptr(), stream=stream, sync=False)
-            return self.image
+            render_native(self.scene, camera, tf, params, self.image.data_ptr(), stream=stream, sync=False,
+                          dev_stats=dev_stats)
+            return (self.image, self.counters) if stats else self.image
         if self.n_local:
             render_native(self.scene, camera, tf, params, self.packed.data_ptr(), tile_rank=self.rank,
-                          tile_world=self.world, stream=stream, sync=False)
-        if not gather:
-            return None
-        self.dist.all_gather_into_tensor(self.gathered, self.packed)
-        if self.rank == 0:
-            N.check(N.lib().xb_unpack_tiles(N.ptr(self.gathered.data_ptr()), self.slots, self.world, self.width,
-                                            self.height, N.ptr(self.image.data_ptr()), N.ptr(stream)))
-            return self.image
-        return None
+                          tile_world=self.world, stream=stream, sync=False, dev_stats=dev_stats)
+        elif stats:
+            self.counters.zero_()
+        img = None
+        if gather:
+            self.exchange()
+            img = self.assemble(stream)
+        if stats:
+            self.reduce_counters()
+            return img, self.counters
+        return img

@@ -279,12 +279,13 @@ def _ensure_device_tree(scene: Scene, mh) -> None:
 
 def render_native(scene: Scene, camera: Camera, tf: TransferFunction, params: MarchParams, out8, outf=None,
                   counts=None, tile_rank=0, tile_world=1, count_bytes=False, stream=None, sync=True,
-                  use_celllocation=False):
+                  use_celllocation=False, dev_stats=None):
     """One `xb_render` call; outputs may be numpy arrays or device pointers (ints).
 
     Returns [regions, samples, algorithmic bytes].  With sync=False and device
-    outputs the call only enqueues work on `stream` (no stats read-back, no
-    host synchronisation) and returns None."""
+    outputs the call only enqueues work on `stream` (no host synchronisation)
+    and returns None; `dev_stats` (device pointer to 3 int64) then receives the
+    counters on the stream."""
     if camera.width < 1 or camera.height < 1:
         raise ValueError("image must be at least 1x1 pixel")
     mh, rh, vh, ih, iso_on = _scene_handles(scene)
@@ -294,9 +295,10 @@ def render_native(scene: Scene, camera: Camera, tf: TransferFunction, params: Ma
         _ensure_device_tree(scene, mh)
     cam = camera_struct(camera)
     m = march_struct(tf, params, scene.iso_value if iso_on else None, use_tree=use_celllocation)
-    stats = np.zeros(3, np.int64) if (sync or count_bytes) else None
+    stats = np.zeros(3, np.int64) if (sync or count_bytes) and dev_stats is None else None
     N.check(N.lib().xb_render(mh.h, rh.h, int(scene.field), vh.h, ih.h if ih else None, C.byref(cam), C.byref(m),
-                              int(tile_rank), int(tile_world), N.ptr(out8), N.ptr(outf), N.ptr(counts), N.ptr(stats),
+                              int(tile_rank), int(tile_world), N.ptr(out8), N.ptr(outf), N.ptr(counts),
+                              N.ptr(stats) if dev_stats is None else C.c_void_p(int(dev_stats)),
                               int(bool(count_bytes)), C.c_void_p(stream) if stream else None))
     return stats
 

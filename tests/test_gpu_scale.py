@@ -1,0 +1,201 @@
+"""GPU parity at the benchmarked scales (BASELINE.json configs[0]-[2]).
+
+* configs[1] (C2, 9.53M cells): GPU builders np.array_equal to the C oracle's
+  (run live), and frame bands of two orbit views within max |dRGBA| <= 1e-3
+  with per-pixel region and sample counters equal.
+* configs[2] (C3, 266M cells): GPU builders against the oracle's sha256
+  digests (tests/golden/scale_digests.json, tools/make_scale_digests.py —
+  the oracle needs ~3 min for it).
+* configs[0] (C1) at its stated 256x256, whole frame.
+* Active sets (T/test_accel.py:111-137): the volume set equals the regions
+  with max_opacity(tf, value_range) > 0 and the iso set the regions with
+  lo <= iso <= hi, for every golden frame's TF, step TFs at value quantiles,
+  and C2.
+"""
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import frame_meta
+from tests_util import sha
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+RGBA_TOL = 1e-3
+MODEL_KEYS = ("brick_lower", "brick_level", "brick_dims", "brick_offset", "scalars")
+REGION_KEYS = ("lo", "hi", "brick_off", "brick_ids", "value_range", "finest_width")
+
+
+def _bench():
+    import sys
+
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    return bench
+
+
+def _build(cells):
+    from paper_2009_03076_b200.bricks import build_bricks
+    from paper_2009_03076_b200.regions import build_regions
+
+    model, _ = build_bricks(cells)
+    return model, build_regions(model)
+
+
+@pytest.fixture(scope="module")
+def c2():
+    bench = _bench()
+    cfg = bench.CONFIGS["c2"]
+    cells = bench.make_cells(cfg)
+    model, regions = _build(cells)
+    return cfg, cells, model, regions
+
+
+def _oracle_scene(model, regions):
+    return oracle.OracleScene({k: getattr(model, k) for k in MODEL_KEYS}, {k: getattr(regions, k) for k in REGION_KEYS})
+
+
+def _ocam(cam):
+    r, u, f = cam.basis()
+    return oracle.camera_struct(cam.width, cam.height, cam.position, r, u, f, math.tan(math.radians(cam.fov_y) * 0.5),
+                                cam.width / cam.height)
+
+
+def test_c2_builders_equal_oracle(c2):
+    cfg, cells, model, regions = c2
+    assert len(cells) == 9_534_568
+    om = oracle.build_bricks(cells.i, cells.j, cells.k, cells.level, cells.values)
+    for k in MODEL_KEYS:
+        assert np.array_equal(getattr(model, k), om[k]), k
+    orr = oracle.build_regions(*(om[k] for k in MODEL_KEYS))
+    for k in REGION_KEYS:
+        assert np.array_equal(getattr(regions, k), orr[k]), k
+
+
+@pytest.mark.parametrize("view", [0, 3])
+def test_c2_frame_bands_match_oracle(c2, view):
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame_float
+
+    bench = _bench()
+    cfg, cells, model, regions = c2
+    tf = bench.tf_for(model.value_range(0), cfg)
+    scene = build_scene(model, regions, tf)
+    cam = bench.cameras_for(regions.bounds, cfg, 8)[view]
+    params = MarchParams(seed=0, gradient_mode="analytic")
+    u8, f64, cnt, stats = render_frame_float(scene, cam, tf, params)
+    osc = _oracle_scene(model, regions)
+    osc.set_tf(tf.domain, tf.rgba)
+    W = cam.width
+    f, c = f64.reshape(-1, 4), cnt.reshape(-1, 2)
+    for y0 in (300, 500, 700):  # three 8-row bands through the volume
+        b, e = y0 * W, (y0 + 8) * W
+        of, ou, pr, ps = osc.render(_ocam(cam), tf.domain, tf.rgba, pix_range=(b, e), seed=0,
+                                    gradient_mode="analytic")
+        assert ps.sum() > 0
+        assert np.abs(f[b:e] - of).max() <= RGBA_TOL, y0
+        assert np.array_equal(c[b:e, 0], pr), y0
+        assert np.array_equal(c[b:e, 1], ps), y0
+        assert np.abs(u8.reshape(-1, 4)[b:e].astype(int) - ou.astype(int)).max() <= 1
+
+
+def test_c2_active_sets_match_enumeration(c2):
+    """T/test_accel.py:111-137 at configs[1] scale."""
+    from paper_2009_03076_b200.accel import TransferFunction, build_iso_bvh, build_volume_bvh
+
+    cfg, cells, model, regions = c2
+    osc = _oracle_scene(model, regions)
+    vr = regions.value_range[:, 0]
+    lo, hi = float(vr.min()), float(vr.max())
+    tfs = [_bench().tf_for((lo, hi), cfg)]
+    for q in (0.3, 0.6, 0.9):  # step TFs opaque above a value quantile (the reference test's construction)
+        cut = float(np.quantile(vr[:, 1], q))
+        a = np.zeros(256)
+        a[int(np.ceil((cut - lo) / (hi - lo) * 255)) + 1:] = 1.0
+        tfs.append(TransferFunction((lo, hi), np.c_[np.ones((256, 3)), a]))
+    for tf in tfs:
+        got = build_volume_bvh(regions, tf, 0, model=model).prims
+        want = osc.active_volume(tf.domain, tf.rgba)
+        assert np.array_equal(np.sort(got), want)
+    for q in (0.1, 0.5, 0.9):
+        iso = float(np.quantile(vr[:, 1], q))
+        got = build_iso_bvh(regions, iso, 0, model=model).prims
+        assert np.array_equal(np.sort(got), osc.active_iso(iso))
+
+
+def test_golden_frame_tfs_active_sets(frames):
+    """Every golden frame's TF (and a mid-range iso value) on its model."""
+    from conftest import golden_digests
+    from paper_2009_03076_b200.accel import TransferFunction, build_iso_bvh, build_volume_bvh
+    from paper_2009_03076_b200.bricks import BrickBuildParams, build_bricks
+    from paper_2009_03076_b200.model import CellList
+    from paper_2009_03076_b200.regions import build_regions
+    from tests_util import golden_cells
+
+    dig = golden_digests()["models"]
+    model_of = {"smoke": "smoke", "ramp": "ramp", "c1": "c1", "aniso": "gauss_aniso"}
+    keys = sorted({k[: -len("_tf_rgba")] for k in frames.files if k.endswith("_tf_rgba")})
+    assert len(keys) >= 12
+    built = {}
+    for key in keys:
+        name = model_of[key.split("_")[0]]
+        if name not in built:
+            i, j, k, lev, vals = golden_cells(name)
+            m, _ = build_bricks(CellList(i, j, k, lev, vals),
+                                BrickBuildParams(max_brick_width=dig[name]["max_brick_width"]))
+            built[name] = (m, build_regions(m))
+        model, regions = built[name]
+        meta = frame_meta(frames, key)
+        tf = TransferFunction(meta["tf_domain"], frames[f"{key}_tf_rgba"])
+        osc = _oracle_scene(model, regions)
+        got = build_volume_bvh(regions, tf, 0, model=model).prims
+        assert np.array_equal(np.sort(got), osc.active_volume(tf.domain, tf.rgba)), key
+        vr = regions.value_range[:, 0]
+        iso = float(0.5 * (vr.min() + vr.max()))
+        got = build_iso_bvh(regions, iso, 0, model=model).prims
+        assert np.array_equal(np.sort(got), osc.active_iso(iso)), key
+
+
+def test_c1_full_frame_256_matches_oracle():
+    """configs[0] at its stated 256x256: the whole frame."""
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame_float
+
+    bench = _bench()
+    cfg = bench.CONFIGS["c1"]
+    cells = bench.make_cells(cfg)
+    assert len(cells) == 97_840
+    model, regions = _build(cells)
+    tf = bench.tf_for(model.value_range(0), cfg)
+    scene = build_scene(model, regions, tf)
+    osc = _oracle_scene(model, regions)
+    osc.set_tf(tf.domain, tf.rgba)
+    for view in (0, 5):
+        cam = bench.cameras_for(regions.bounds, cfg, 8)[view]
+        assert (cam.width, cam.height) == (256, 256)
+        params = MarchParams(seed=0, gradient_mode="analytic")
+        u8, f64, cnt, stats = render_frame_float(scene, cam, tf, params)
+        of, ou, pr, ps = osc.render(_ocam(cam), tf.domain, tf.rgba, seed=0, gradient_mode="analytic")
+        assert np.abs(f64 - of).max() <= RGBA_TOL
+        assert np.array_equal(cnt[..., 0].ravel(), pr) and np.array_equal(cnt[..., 1].ravel(), ps)
+        assert int(stats[1]) == int(ps.sum()) and int(stats[0]) == int(pr.sum())
+
+
+def test_c3_builders_match_oracle_digests():
+    """configs[2] (266M cells): every GPU builder array has the oracle's sha256."""
+    bench = _bench()
+    gold = json.loads((ROOT / "tests" / "golden" / "scale_digests.json").read_text())["c3"]
+    cells = bench.make_cells(bench.CONFIGS["c3"])
+    assert len(cells) == gold["n_cells"]
+    for a in ("i", "j", "k", "level", "values"):
+        assert sha(getattr(cells, a)) == gold["cells"][a], a
+    model, regions = _build(cells)
+    del cells
+    for k in MODEL_KEYS:
+        assert sha(getattr(model, k)) == gold["model"][k], k
+    for k in REGION_KEYS:
+        assert sha(getattr(regions, k)) == gold["regions"][k], k

@@ -229,3 +229,35 @@ def test_tiles_partition_every_pixel_once(W, H, world):
         x, y, valid = packed_pixel_coords(W, H, r, world)
         np.add.at(seen, (y[valid], x[valid]), 1)
     assert (seen == 1).all()
+
+
+def test_parallel_generator_equals_serial():
+    """generate_synthetic(workers=N) splits the frontier into chunks: same arrays, same order."""
+    from paper_2009_03076_b200 import io as xio
+
+    spec = xio.SyntheticSpec(field="gaussian", extent=(16384, 8192, 8192), max_level=12, threshold=0.05, seed=0,
+                             holes=((6144.0, 6144.0, 6144.0, 40.0),), refine_spheres=((6144.0, 6144.0, 6144.0, 90.0),),
+                             field_params={"center": (6144.0, 6144.0, 6144.0), "sigma": 600.0})
+    a = xio.generate_synthetic(spec)
+    b = xio.generate_synthetic(spec, workers=4)
+    assert len(a) > (1 << 16)
+    for k in ("i", "j", "k", "level", "values"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_scale_digest_fixture_pins_c2_cells():
+    """tests/golden/scale_digests.json was made from the numpy generator's cells (the C2 entry is cheap to redo)."""
+    import json
+    import sys
+
+    from tests_util import sha
+
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    d = json.loads((ROOT / "tests" / "golden" / "scale_digests.json").read_text())
+    assert {"c2", "c3"} <= set(d)
+    cells = bench.make_cells(bench.CONFIGS["c2"])
+    assert len(cells) == d["c2"]["n_cells"]
+    for a in ("i", "j", "k", "level", "values"):
+        assert sha(getattr(cells, a)) == d["c2"]["cells"][a], a

@@ -1,9 +1,10 @@
-"""World-size-2 CPU test of the screen-tile exchange (gloo stands in for NCCL).
+"""World-size-2 CPU tests of the screen-tile exchange (gloo stands in for NCCL).
 
-Each rank fills its packed tile buffer with a deterministic function of the
-global pixel index (what the kernel's global-pixel rho hash guarantees), the
-buffers are all-gathered exactly as `TiledRenderer.render` does, and rank 0's
-unpacked image must equal the single-rank frame."""
+Each rank fills its TiledRenderer's packed tile buffer with a deterministic
+function of the global pixel index (what the kernel's global-pixel rho hash
+guarantees); `TiledRenderer.exchange()` all-gathers the buffers and
+`reduce_counters()` sums the frame counters, exactly as `render()` does on the
+GPU, and rank 0's unpacked image must equal the single-rank frame."""
 import os
 import socket
 
@@ -31,20 +32,38 @@ def _pixel_value(x, y, W):
 def _worker(rank, world, port, W, H, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2009_03076_b200.parallel import TILE_PX, packed_pixel_coords, tiles_per_rank, unpack_host
+    from paper_2009_03076_b200.parallel import TILE_PX, TiledRenderer, packed_pixel_coords, unpack_host
 
-    slots = tiles_per_rank(W, H, world)
-    packed = np.zeros((slots * TILE_PX, 4), np.uint8)
+    # TiledRenderer's own exchange / counter reduction on CPU tensors; the
+    # device render is stood in for by writing this rank's tiles directly
+    rend = TiledRenderer(scene=None, width=W, height=H, device=torch.device("cpu"))
     x, y, valid = packed_pixel_coords(W, H, rank, world)
+    packed = rend.packed.numpy()
     packed[: len(x)][valid] = _pixel_value(x[valid], y[valid], W)
-    t = torch.from_numpy(packed)
-    parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t)
-    counts = torch.tensor([int(valid.sum())], dtype=torch.int64)
-    dist.all_reduce(counts)
+    rend.counters[:] = torch.tensor([int(valid.sum()), 10 * int(valid.sum()), 0])
+    g = rend.exchange()
+    c = rend.reduce_counters()
     if rank == 0:
-        img = unpack_host([p.numpy() for p in parts], W, H, world)
-        out_q.put((img, int(counts.item())))
+        parts = g.numpy().reshape(world, rend.slots * TILE_PX, 4)
+        img = unpack_host(list(parts), W, H, world)
+        out_q.put((img, int(c[0]), int(c[1])))
+    dist.destroy_process_group()
+
+
+def _camera_check(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2009_03076_b200.parallel import TiledRenderer
+
+    class Cam:
+        width, height = 64, 32
+
+    rend = TiledRenderer(scene=None, width=48, height=32, device=torch.device("cpu"))
+    try:
+        rend.render(Cam(), None, None)
+        out_q.put("no error")
+    except ValueError as e:
+        out_q.put(str(e))
     dist.destroy_process_group()
 
 
@@ -56,11 +75,25 @@ def test_tile_gather_world2_matches_single_frame(W, H):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, W, H, q)) for r in range(2)]
     for p in procs:
         p.start()
-    img, n = q.get(timeout=120)
+    img, n, n10 = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     yy, xx = np.mgrid[0:H, 0:W]
     want = _pixel_value(xx.ravel(), yy.ravel(), W).reshape(H, W, 4)
-    assert n == W * H
+    assert n == W * H and n10 == 10 * W * H  # counters summed over the ranks
     assert np.array_equal(img, want)
+
+
+def test_tiled_renderer_rejects_camera_of_another_size():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_camera_check, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    msgs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all("renderer was built for 48x32" in m for m in msgs), msgs
