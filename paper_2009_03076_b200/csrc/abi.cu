@@ -239,6 +239,7 @@ int xb_build_bricks(const int32_t* i, const int32_t* j, const int32_t* k, const 
                     xb_model** out) {
     *out = nullptr;
     return guarded([&] {
+        xb::NvtxRange nvtx_range("xb_build_bricks");
         XB_CHECK(n >= 0 && n_fields >= 1, XB_ERR_ARG, "bad cell counts");
         xb::DeviceGuard g(device);
         OwnedStream st;
@@ -253,6 +254,7 @@ int xb_build_bricks(const int32_t* i, const int32_t* j, const int32_t* k, const 
 int xb_generate_synthetic(const xb_synth_spec* spec, int32_t device, xb_cells** out) {
     *out = nullptr;
     return guarded([&] {
+        xb::NvtxRange nvtx_range("xb_generate_synthetic");
         XB_CHECK(spec != nullptr, XB_ERR_ARG, "null spec");
         xb::DeviceGuard g(device);
         OwnedStream st;
@@ -321,6 +323,7 @@ int xb_cells_upload(xb_cells* c, int64_t offset, int64_t count, const int32_t* i
 int xb_build_bricks_cells(const xb_cells* c, int32_t max_brick_width, int32_t keep_split_tree, xb_model** out) {
     *out = nullptr;
     return guarded([&] {
+        xb::NvtxRange nvtx_range("xb_build_bricks (device cells)");
         XB_CHECK(c != nullptr, XB_ERR_ARG, "null cells");
         xb::DeviceGuard g(c->c.device);
         OwnedStream st;
@@ -442,6 +445,7 @@ void xb_model_free(xb_model* m) {
 int xb_build_regions(const xb_model* m, xb_regions** out) {
     *out = nullptr;
     return guarded([&] {
+        xb::NvtxRange nvtx_range("xb_build_regions");
         XB_CHECK(m, XB_ERR_ARG, "null model");
         xb::DeviceGuard g(m->m.device);
         OwnedStream st;
@@ -492,6 +496,7 @@ static int make_active(const xb_regions* r, int kind, int32_t field, double lo, 
                        double iso, xb_active** out) {
     *out = nullptr;
     return guarded([&] {
+        xb::NvtxRange nvtx_range(kind == 0 ? "active set: volume majorants" : (kind == 1 ? "active set: iso" : "active set: all"));
         XB_CHECK(r, XB_ERR_ARG, "null regions");
         if (kind == 0) XB_CHECK(rgba && lo < hi, XB_ERR_ARG, "transfer function domain must satisfy lo < hi");
         xb::DeviceGuard g(r->r.device);

@@ -9,6 +9,7 @@
 //   k-d tree : KdNode[T] (8 B): BFS order, children adjacent; leaves carry the
 //              region id (or -1 for a cavity outside the support union)
 #pragma once
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without a profiler attached
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -197,6 +198,14 @@ struct DevRegions {
     // reference-layout arrays for download
     DevBuf<double> lo, hi, finest, vr64;
     DevBuf<int64_t> brick_off;
+};
+
+// host-side NVTX range for the phases of a call (visible in nsys / ncu --nvtx)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 }  // namespace xb

@@ -1527,6 +1527,7 @@ static void hit_select(const RenderArgs& A, int64_t n_slots, cudaStream_t s) {
 
 void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaStream_t s) {
     if (n_tiles_local <= 0) return;
+    NvtxRange frame_range("xb_render: frame");
     const bool iso = A.M.iso_on != 0;
     const int g = grad_index(A.M.grad_mode);
     const int64_t n_slots = n_tiles_local * kTileW * kTileH;
@@ -1536,6 +1537,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         XB_CUDA(cudaLaunchKernel(fn, dim3(grid_for(n_slots, 128)), dim3(128), args, 0, s));
     } else if (iso) {
         // iso phase through the walk machinery: classify, select, walk the iso set, march
+        NvtxRange r_iso("iso phase: classify, select, walk, route, k_iso_warp");
         RenderArgs* Ai = new RenderArgs(A);
         std::unique_ptr<RenderArgs> hold(Ai);
         Ai->walk_iso = 1;
@@ -1587,6 +1589,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             // C2 6.30 / 6.30 / 6.27 / 6.42, C3 flat)
             W.walk_tau_stop = (float)(-std::log(1.0 - e));
             void* wargs[] = {(void*)&A, (void*)&n_slots};
+            NvtxRange r_walk("walk phase: k_classify, hit select, k_walk, k_route, k_walk2");
             XB_CUDA(cudaLaunchKernel((const void*)k_classify, dim3(grid_for(n_slots, kWalkThreads)),
                                      dim3(kWalkThreads), wargs, 0, s));
             hit_select(A, n_slots, s);
@@ -1627,6 +1630,7 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), want));
     void* args[] = {(void*)&A, (void*)&n_slots};
     cudaEvent_t* ev = (cudaEvent_t*)A.march_events;
+    NvtxRange r_march("march: k_warp");
     if (ev) XB_CUDA(cudaEventRecord(ev[0], s));
     XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(threads), args, dyn, s));
     if (ev) XB_CUDA(cudaEventRecord(ev[1], s));

@@ -21,7 +21,7 @@ def _run(*args):
 
 @pytest.mark.gpu
 def test_bench_line_contract():
-    d = _run("--config", "c1", "--secondary", "", "--steps", "3", "--warmup", "3", "--cpu-seconds", "1")
+    d = _run("--config", "c1", "--secondary", "", "--extra", "", "--steps", "3", "--warmup", "3", "--cpu-seconds", "1")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"):
         assert k in d, k
@@ -38,13 +38,32 @@ def test_bench_line_contract():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] >= 4 * 256 * 256
     assert d["gpu_launches"] >= 5 * d["steps"]
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    # parity measured in the run: the oracle's bands of orbit view 0 against the GPU frame
+    p = d["parity"]
+    assert p["ok"] is True and p["frame"]["max_abs_drgba"] <= 1e-3
+    assert p["frame"]["px_region_counter_mismatches"] == 0 and p["frame"]["px_sample_counter_mismatches"] == 0
+    assert len(d["views"]) == d["config"]["views"] == 8
+    assert r["kernel"].startswith("k_warp") and r["frame_achieved"] <= r["achieved"]
 
 
 @pytest.mark.gpu
 def test_bench_reference_arm_contract():
-    d = _run("--impl", "reference", "--config", "c1", "--secondary", "", "--steps", "1", "--warmup", "1",
-             "--cpu-seconds", "1")
+    d = _run("--impl", "reference", "--config", "c1", "--secondary", "", "--extra", "", "--steps", "1",
+             "--warmup", "1", "--cpu-seconds", "1")
     assert d["impl"] == "reference"
     assert d["value"] > 0 and d["unit"] == "frames/s"
     assert d["cpu_baseline"]["kind"] in ("port", "reference")
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    ours = _run("--config", "c1", "--secondary", "", "--extra", "", "--steps", "1", "--warmup", "1",
+                "--no-cpu-baseline", "--no-ablations")
+    assert d["config"] == ours["config"]  # same workload, same keys: the driver's same_config
+
+
+def test_reference_arm_loads_no_gpu_library():
+    """The reference arm runs host code only: libexabricks.so is never mapped."""
+    code = ("import sys, runpy; sys.argv=['bench.py','--impl','reference','--config','c1','--steps','1',"
+            "'--warmup','1']; import bench; bench.main(sys.argv[1:]);"
+            "maps=open('/proc/self/maps').read(); print('LIB', 'libexabricks' in maps)")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "LIB False" in out.stdout

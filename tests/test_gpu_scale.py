@@ -139,7 +139,7 @@ def test_golden_frame_tfs_active_sets(frames):
 
     dig = golden_digests()["models"]
     model_of = {"smoke": "smoke", "ramp": "ramp", "c1": "c1", "aniso": "gauss_aniso"}
-    keys = sorted({k[: -len("_tf_rgba")] for k in frames.files if k.endswith("_tf_rgba")})
+    keys = sorted({k[: -len("_tf_rgba")] for k in frames if k.endswith("_tf_rgba")})
     assert len(keys) >= 12
     built = {}
     for key in keys:
