@@ -201,6 +201,9 @@ int xb_sample_points(const xb_model* m, const xb_regions* r, int32_t field, int6
                      const int32_t* region, int32_t want_grad, int32_t* region_out, double* acc);
 /* basis_sample_oracle over the canonical cell order (R/sampling.py:291-298): out (n,2) num, den */
 int xb_sample_scan(const xb_model* m, int32_t field, int64_t n, const double* p, double* out);
+/* the same scan over any device cell list in its given order (basis_sample_oracle on a plain
+ * CellList, R/sampling.py:291-298; one field, uploaded with xb_cells_create / xb_cells_upload) */
+int xb_sample_scan_cells(const xb_cells* c, int64_t n, const double* p, double* out);
 /* iterate_intervals R/accel.py:414-424 for n rays: up to cap intervals each (t_in, t_out, region), count */
 int xb_trace_intervals(const xb_model* m, const xb_regions* r, const xb_active* a, int64_t n, const double* o,
                        const double* d, double t_start, double t_max, int32_t cap, double* t_in, double* t_out,

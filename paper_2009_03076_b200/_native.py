@@ -100,6 +100,7 @@ SIGNATURES = {
     "xb_iso_rays": (C.c_int, [P, P, i32, P, P, i64, P, P, P, P, P, P, P]),
     "xb_sample_points": (C.c_int, [P, P, i32, i64, P, P, i32, P, P]),
     "xb_sample_scan": (C.c_int, [P, i32, i64, P, P]),
+    "xb_sample_scan_cells": (C.c_int, [P, i64, P, P]),
     "xb_trace_intervals": (C.c_int, [P, P, P, i64, P, P, f64, f64, i32, P, P, P, P]),
     "xb_active_lbvh_info": (C.c_int, [P, P, P, P]),
     "xb_active_lbvh_download": (C.c_int, [P, P, P, P, P, P, P, P]),

@@ -24,6 +24,11 @@ struct xb_cells {
 };
 struct xb_model {
     xb::DevModel m;
+    // the frame gather's padded copy of each rendered field (march.cuh:kGatherPad), built
+    // on the field's first render and kept for the model's life (concurrent renders
+    // of other fields never see it move)
+    mutable std::mutex gv_mu;
+    mutable std::vector<std::unique_ptr<xb::DevBuf<float>>> gvals;
 };
 struct xb_regions {
     xb::DevRegions r;
@@ -78,18 +83,24 @@ struct OwnedStream {
     }
 };
 
-// keep freed stream-ordered allocations in the device pool (per-frame scratch
-// of up to a few GB is reused every frame instead of going back to the driver)
+// keep up to 8 GB of freed stream-ordered allocations in the device pool: a
+// frame's scratch (<= ~4 GB, see kBandSlots) is reused every frame instead of
+// going back to the driver, while larger or concurrent peaks are released at
+// the next synchronisation instead of being held for the life of the process
 void keep_pool(int device) {
-    static bool done[64] = {};
-    if (device < 0 || device >= 64 || done[device]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done[device] = true;
+    static std::once_flag done[64];
+    if (device < 0 || device >= 64) return;
+    std::call_once(done[device], [device] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = 8ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
 }
+
+// pixels rendered per pass; larger frames run as interleaved tile bands (xb_render)
+constexpr int64_t kBandSlots = 1ll << 22;
 
 // frame-gather brick records in region-list order (march.cuh:RbRec)
 __global__ void k_region_bricks(const int32_t* __restrict__ ids, int64_t n, const int4* __restrict__ ba,
@@ -122,6 +133,24 @@ void ensure_region_bricks(const xb_model* m, const xb_regions* r) {
     r->rb_ok = true;
 }
 
+// the field's values with kGatherPad zeros on both sides (march.cuh:brick_step)
+const float* gather_values(const xb_model* m, int field) {
+    std::lock_guard<std::mutex> g(m->gv_mu);
+    if ((int)m->gvals.size() <= field) m->gvals.resize(field + 1);
+    if (!m->gvals[field]) {
+        const int64_t n = m->m.n_cells, pad = xb::kGatherPad;
+        auto b = std::make_unique<xb::DevBuf<float>>((size_t)(n + 2 * pad));
+        OwnedStream st;
+        XB_CUDA(cudaMemsetAsync(b->p, 0, (size_t)(n + 2 * pad) * sizeof(float), st.s));
+        if (n)
+            XB_CUDA(cudaMemcpyAsync(b->p + pad, m->m.vals.p + (size_t)field * (size_t)n, (size_t)n * sizeof(float),
+                                    cudaMemcpyDeviceToDevice, st.s));
+        XB_CUDA(cudaStreamSynchronize(st.s));
+        m->gvals[field] = std::move(b);
+    }
+    return m->gvals[field]->p + xb::kGatherPad;
+}
+
 xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     XB_CHECK(m && r, XB_ERR_ARG, "null model or regions");
     XB_CHECK(r->model_bricks == m->m.n_bricks, XB_ERR_ARG, "regions were built for a different model");
@@ -132,6 +161,7 @@ xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     S.brick_a = m->m.brick_a.p;
     S.brick_m = m->m.brick_m.p;
     S.vals = m->m.vals.p + (size_t)field * (size_t)m->m.n_cells;
+    S.gvals = gather_values(m, field);
     S.rec = r->r.rec.p;
     S.rids = r->r.ids.p;
     ensure_region_bricks(m, r);
@@ -647,6 +677,41 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         const xb_tuning T = tuning_snapshot();
         xb::DeviceGuard g(m->m.device);
         cudaStream_t s = (cudaStream_t)stream;
+        const int64_t frame_px = (int64_t)cam->width * cam->height;
+        if (tile_world == 1 && !rgba_f64 && !px_counts && frame_px > kBandSlots) {
+            // Large frames render as interleaved tile bands of <= kBandSlots pixels (the
+            // multi-GPU tile split, on one device), so the per-pixel walk scratch (~1 KB per
+            // pixel in flight) stays bounded whatever the resolution; then one unpack.
+            const int bands = (int)((frame_px + kBandSlots - 1) / kBandSlots);
+            const int64_t tpr = tiles_for_rank(cam->width, cam->height, 0, bands, nullptr, nullptr);
+            const int64_t band_px = tpr * xb::kTileW * xb::kTileH;
+            OutBuf<uchar4> img;
+            img.setup((uchar4*)rgba8, (size_t)frame_px, s);
+            uchar4* packed = nullptr;
+            int64_t* dst = nullptr;
+            XB_CUDA(cudaMallocAsync((void**)&packed, (size_t)bands * band_px * sizeof(uchar4), s));
+            XB_CUDA(cudaMallocAsync((void**)&dst, (size_t)bands * 3 * sizeof(int64_t), s));
+            for (int b = 0; b < bands; b++) {
+                const int rc = xb_render(m, r, field, vol, iso, cam, mp, b, bands, packed + (size_t)b * band_px,
+                                         nullptr, nullptr, dst + 3 * b, count_bytes, stream);
+                if (rc != XB_OK) throw xb::Error(rc, g_err);
+            }
+            int tx, ty;
+            tiles_for_rank(cam->width, cam->height, 0, 1, &tx, &ty);
+            xb::launch_unpack(packed, tpr, bands, tx, ty, cam->width, cam->height, img.dev, s);
+            img.finish();
+            std::vector<int64_t> hs((size_t)bands * 3);
+            if (stats) XB_CUDA(cudaMemcpyAsync(hs.data(), dst, hs.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            XB_CUDA(cudaFreeAsync(packed, s));
+            XB_CUDA(cudaFreeAsync(dst, s));
+            XB_CUDA(cudaStreamSynchronize(s));
+            if (stats) {
+                stats[0] = stats[1] = stats[2] = 0;
+                for (int b = 0; b < bands; b++)
+                    for (int q = 0; q < 3; q++) stats[q] += hs[3 * b + q];
+            }
+            return;
+        }
         xb::RenderArgs* A = new xb::RenderArgs();  // 8.6 KB: keep off the stack
         std::unique_ptr<xb::RenderArgs> hold(A);
         A->S = scene_view(m, r, field);
@@ -915,6 +980,20 @@ int xb_sample_scan(const xb_model* m, int32_t field, int64_t n, const double* p,
         dp.upload(p, 3 * n, st.s);
         dout.alloc(2 * n + 1);
         xb::sample_scan(S, m->m.n_bricks, n, dp.p, dout.p, st.s);
+        dout.download(out, 2 * n, st.s);
+        XB_CUDA(cudaStreamSynchronize(st.s));
+    });
+}
+
+int xb_sample_scan_cells(const xb_cells* c, int64_t n, const double* p, double* out) {
+    return guarded([&] {
+        XB_CHECK(c && n >= 0, XB_ERR_ARG, "bad arguments");
+        xb::DeviceGuard g(c->c.device);
+        OwnedStream st;
+        xb::DevBuf<double> dp, dout;
+        dp.upload(p, 3 * n, st.s);
+        dout.alloc(2 * n + 1);
+        xb::scan_cells(c->c.i.p, c->c.j.p, c->c.k.p, c->c.level.p, c->c.vals.p, c->c.n, n, dp.p, dout.p, st.s);
         dout.download(out, 2 * n, st.s);
         XB_CUDA(cudaStreamSynchronize(st.s));
     });

@@ -257,6 +257,70 @@ __global__ void k_sample_scan(SceneView S, int64_t n_bricks, int64_t n, const do
     }
 }
 
+// `_accumulate_cells` (R/sampling.py:106-120) over an arbitrary cell list in its
+// given order (basis_sample_oracle on a plain CellList, R/sampling.py:291-298):
+// one block per point; each pass tests 128 consecutive cells (hats > 0), a
+// block scan of the hit flags appends the contributing indices in list order
+// to shared memory, and one thread adds them in that order — the reference's
+// exact sequence.  A point with more than kScanCap contributors (not possible
+// for a valid AMR list, whose cells are disjoint) takes the sequential scan.
+constexpr int kScanCap = 1024;
+__global__ void __launch_bounds__(128) k_scan_cells(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
+                                                     const int32_t* __restrict__ ck, const int32_t* __restrict__ cl,
+                                                     const float* __restrict__ cv, int64_t n_cells, int64_t n,
+                                                     const double* __restrict__ p, double* __restrict__ out) {
+    __shared__ int32_t s_hit[kScanCap];
+    __shared__ int s_warp[4];
+    __shared__ int s_n;
+    const int64_t q = blockIdx.x;
+    if (q >= n) return;
+    const double px = p[3 * q], py = p[3 * q + 1], pz = p[3 * q + 2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    auto hats = [&](int64_t t, double& hx, double& hy, double& hz) {
+        const double w = pow2(cl[t]), iw = pow2(-cl[t]);
+        hx = 1.0 - fabs(((double)ci[t] + 0.5 * w) - px) * iw;
+        hy = 1.0 - fabs(((double)cj[t] + 0.5 * w) - py) * iw;
+        hz = 1.0 - fabs(((double)ck[t] + 0.5 * w) - pz) * iw;
+    };
+    for (int64_t base = 0; base < n_cells; base += blockDim.x) {
+        const int64_t t = base + threadIdx.x;
+        bool hit = false;
+        if (t < n_cells) {
+            double hx, hy, hz;
+            hats(t, hx, hy, hz);
+            hit = hx > 0.0 && hy > 0.0 && hz > 0.0;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) s_warp[wid] = __popc(b);
+        __syncthreads();
+        int before = s_n;
+        for (int w = 0; w < wid; w++) before += s_warp[w];
+        const int pos = before + __popc(b & ((1u << lane) - 1u));
+        if (hit && pos < kScanCap) s_hit[pos] = (int32_t)t;
+        __syncthreads();
+        if (threadIdx.x == 0) s_n += s_warp[0] + s_warp[1] + s_warp[2] + s_warp[3];
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    double num = 0.0, den = 0.0;
+    const bool fits = s_n <= kScanCap;
+    const int64_t m = fits ? s_n : n_cells;
+    for (int64_t u = 0; u < m; u++) {
+        const int64_t t = fits ? s_hit[u] : u;
+        double hx, hy, hz;
+        hats(t, hx, hy, hz);
+        if (hx > 0.0 && hy > 0.0 && hz > 0.0) {
+            const double h = hx * hy * hz;
+            num += h * (double)cv[t];
+            den += h;
+        }
+    }
+    out[2 * q] = num;
+    out[2 * q + 1] = den;
+}
+
 // iterate_intervals (R/accel.py:414-424) for a batch of rays, via the ordered
 // k-d walk; up to `cap` intervals per ray.
 __global__ void k_trace(SceneView S, const uint8_t* __restrict__ flags, int64_t n, const double* __restrict__ o,
@@ -311,6 +375,15 @@ void sample_scan(const SceneView& S, int64_t n_bricks, int64_t n, const double* 
         check_launch("k_sample_scan");
     }
     XB_CUDA(cudaStreamSynchronize(s));
+}
+
+void scan_cells(const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* l, const float* v, int64_t n_cells,
+                int64_t n, const double* p, double* out, cudaStream_t s) {
+    for (int64_t b = 0; b < n; b += 65535) {
+        const int64_t m = std::min<int64_t>(65535, n - b);
+        k_scan_cells<<<(unsigned)m, 128, 0, s>>>(i, j, k, l, v, n_cells, m, p + 3 * b, out + 2 * b);
+        check_launch("k_scan_cells");
+    }
 }
 
 void trace_intervals(const SceneView& S, const uint8_t* flags, int64_t n, const double* o, const double* d, double t0,

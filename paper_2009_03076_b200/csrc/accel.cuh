@@ -33,6 +33,8 @@ void build_active(const DevRegions& R, int kind, int field, double tf_lo, double
 
 void sample_points(const SceneView& S, int64_t n, const double* p, const int32_t* rid_in, int want_grad, int32_t* rid_out,
                    double* out, cudaStream_t s);
+void scan_cells(const int32_t* i, const int32_t* j, const int32_t* k, const int32_t* l, const float* v, int64_t n_cells,
+                int64_t n, const double* p, double* out, cudaStream_t s);
 void sample_scan(const SceneView& S, int64_t n_bricks, int64_t n, const double* p, double* out, cudaStream_t s);
 void trace_intervals(const SceneView& S, const uint8_t* flags, int64_t n, const double* o, const double* d, double t0,
                      double t1, int cap, double* tin, double* tout, int32_t* reg, int32_t* cnt, cudaStream_t s,

@@ -23,7 +23,13 @@ namespace xb {
 
 constexpr double kEpsWeight = 1e-12;     // EPS_WEIGHT, R/sampling.py:37
 
-constexpr double kTFar = 1.0e30;         // _T_FAR, R/render.py:49
+#ifndef XB_INT_TESTS
+#define XB_INT_TESTS 1
+#endif
+constexpr double kTFar = 1.0e30;
+// zero pad around the frame gather's value copy: a brick's unclamped 2x2x2
+// window reaches at most nx*(ny+1) + 1 <= 32*33 + 1 values before or after it
+constexpr int64_t kGatherPad = 2048;         // _T_FAR, R/render.py:49
 constexpr int kKdStack = 64;
 
 // exact power of two for |e| < 1022 (brick cell widths, finest widths)
@@ -84,6 +90,8 @@ struct SceneView {
     const int4* __restrict__ brick_a;
     const uint32_t* __restrict__ brick_m;
     const float* __restrict__ vals;
+    // the frame gather's copy of the field: vals with kGatherPad zeros before and after
+    const float* __restrict__ gvals;
     const RegionRec* __restrict__ rec;
     const int32_t* __restrict__ rids;
     // frame-gather brick records in region-list order (rb[i] = brick rids[i]):
@@ -625,12 +633,23 @@ __device__ __forceinline__ Axis2 window_axis(double p, double l, int n, double w
     const double c0 = __fma_rn((double)A.x0 + 0.5, w, l);  // exact: l + (x0 + 1/2) w
     const double e0 = c0 - p, e1 = (c0 + w) - p;
     const double h0 = __fma_rn(-fabs(e0), iw, 1.0), h1 = __fma_rn(-fabs(e1), iw, 1.0);
+#if XB_INT_TESTS
+    // sign tests on the high words (integer pipe; the FP64 pipe is the gather's
+    // bottleneck).  For a double x that is 0, normal, or negative, x > 0.0 <=> its
+    // high word is > 0 as a signed int; subnormal h or e cannot occur here (h is
+    // 0 or >= 2^-53, e a difference of doubles ~ the coordinates' magnitude)
+    A.v0 = (unsigned)A.x0 < (unsigned)n && __double2hiint(h0) > 0;
+    A.v1 = (unsigned)(A.x0 + 1) < (unsigned)n && __double2hiint(h1) > 0;
+    A.s0 = A.v0 ? (__double2hiint(e0) > 0 ? fw : -fw) : 0.f;
+    A.s1 = A.v1 ? (__double2hiint(e1) > 0 ? fw : -fw) : 0.f;
+#else
     A.v0 = (unsigned)A.x0 < (unsigned)n && h0 > 0.0;
     A.v1 = (unsigned)(A.x0 + 1) < (unsigned)n && h1 > 0.0;
-    A.h0 = A.v0 ? h0 : 0.0;
-    A.h1 = A.v1 ? h1 : 0.0;
     A.s0 = A.v0 ? (e0 > 0.0 ? fw : -fw) : 0.f;
     A.s1 = A.v1 ? (e1 > 0.0 ? fw : -fw) : 0.f;
+#endif
+    A.h0 = A.v0 ? h0 : 0.0;
+    A.h1 = A.v1 ? h1 : 0.0;
     return A;
 }
 
@@ -650,17 +669,20 @@ __device__ __forceinline__ void brick_step(const SceneView& S, const RbRec& B, d
     const Axis2 Y = window_axis(py, B.ly, ny, w, iw, fw);
     const Axis2 Z = window_axis(pz, B.lz, nz, w, iw, fw);
     A.n_nz += ((int)X.v0 + (int)X.v1) * ((int)Y.v0 + (int)Y.v1) * ((int)Z.v0 + (int)Z.v1);
-    const int xa = max(X.x0, 0), xb = min(X.x0 + 1, nx - 1);
-    const int ya = max(Y.x0, 0), yb = min(Y.x0 + 1, ny - 1);
-    const int za = max(Z.x0, 0), zb = min(Z.x0 + 1, nz - 1);
-    const float* __restrict__ base = S.vals + B.off;
-    const int r00 = nx * (ya + ny * za), r01 = nx * (yb + ny * za), r10 = nx * (ya + ny * zb),
-              r11 = nx * (yb + ny * zb);
+    // The 2x2x2 window is read unclamped from S.gvals, the field's values with
+    // kGatherPad zeros on both sides: an out-of-brick slot reads a finite
+    // neighbour (or a pad zero) that its zero hat cancels exactly, so the eight
+    // addresses are one pointer and three strides (+1 is an immediate offset).
+    // The clamp to [-1, n-1] only keeps a corrupt window inside the pads.
+    const int x0 = min(max(X.x0, -1), nx - 1), y0 = min(max(Y.x0, -1), ny - 1), z0 = min(max(Z.x0, -1), nz - 1);
+    const int sy = nx, sz = nx * ny;
+    const float* __restrict__ p0 = S.gvals + B.off + (x0 + nx * y0 + sz * z0);
+    const float* __restrict__ p1 = p0 + sz;
     float vv[2][2][2];  // [dz][dy][dx]
-    vv[0][0][0] = __ldg(base + (r00 + xa)); vv[0][0][1] = __ldg(base + (r00 + xb));
-    vv[0][1][0] = __ldg(base + (r01 + xa)); vv[0][1][1] = __ldg(base + (r01 + xb));
-    vv[1][0][0] = __ldg(base + (r10 + xa)); vv[1][0][1] = __ldg(base + (r10 + xb));
-    vv[1][1][0] = __ldg(base + (r11 + xa)); vv[1][1][1] = __ldg(base + (r11 + xb));
+    vv[0][0][0] = __ldg(p0); vv[0][0][1] = __ldg(p0 + 1);
+    vv[0][1][0] = __ldg(p0 + sy); vv[0][1][1] = __ldg(p0 + sy + 1);
+    vv[1][0][0] = __ldg(p1); vv[1][0][1] = __ldg(p1 + 1);
+    vv[1][1][0] = __ldg(p1 + sy); vv[1][1][1] = __ldg(p1 + sy + 1);
     // the reference's sequence: h = (hx*hy)*hz, cells z, y, x ascending
     const double hxy00 = X.h0 * Y.h0, hxy01 = X.h1 * Y.h0, hxy10 = X.h0 * Y.h1, hxy11 = X.h1 * Y.h1;  // [dy][dx]
     const double hzz[2] = {Z.h0, Z.h1};

@@ -134,7 +134,10 @@ __global__ void __launch_bounds__(128) k_iso_pass(const __grid_constant__ Render
 // the reference by rounding only (~1e-16), like CUDA's pow.
 
 constexpr int kWarpThreads = 128;
-constexpr int kWarpMinBlocks = 4;
+#ifndef XB_WARP_MINB
+#define XB_WARP_MINB 4
+#endif
+constexpr int kWarpMinBlocks = XB_WARP_MINB;
 constexpr int kWarpsPerBlock = kWarpThreads / 32;
 constexpr int kWarpStack = 256;  // spilled frontier entries per warp
 constexpr int kRaysPerGrab = 8;  // rays taken per work-counter atomic
@@ -1374,7 +1377,9 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         }
                         const double t_last = __shfl_sync(FULL, g_co, ns - 1);
                         const int S_new = __shfl_sync(FULL, P, 31);
-                        // append: new segment i -> window position nq + i
+                        // append: new segment i -> window position nq + i (a ring slot the last
+                        // chunk may still have been reading: order the warp's reads first)
+                        __syncwarp();
                         if (lane < ns) {
                             SegQ& q = ring[(qh + nq + lane) & 31];
                             q.ci = g_ci; q.co = g_co; q.kf = g_kf;

@@ -136,20 +136,35 @@ def basis_sample_region(p, region, model: AmrModel, field: int = 0, regions=None
 
 
 def basis_sample_oracle(p, cells, field: int = 0, model: AmrModel | None = None) -> SampleResult:
-    """Linear scan over every cell in canonical order (R/sampling.py:291-298), on the GPU.
+    """Linear scan over every cell, in the list's own order (R/sampling.py:291-298), on the GPU.
 
-    The scan is over `model`'s canonical cell list; `cells` must be that list
-    (`model.cell_list()`), as in the reference's tests.
+    A model's canonical list (`model.cell_list()`, or `model=` given) is scanned
+    from the resident model; any other CellList is uploaded and scanned in its
+    given order (`xb_sample_scan_cells`) — the reference's exact running sums
+    either way.
     """
-    model = model if model is not None else getattr(cells, "_model", None)
-    if model is None:
-        raise ValueError("basis_sample_oracle needs the AmrModel whose cell_list() is scanned")
-    from .bricks import model_handle
+    import ctypes as C
 
-    mh = model_handle(model)
+    model = model if model is not None else getattr(cells, "_model", None)
     pts = np.ascontiguousarray(np.asarray(p, np.float64).reshape(-1, 3))
     out = np.empty((len(pts), 2))
-    N.check(N.lib().xb_sample_scan(mh.h, int(field), len(pts), N.ptr(pts), N.ptr(out)))
+    if model is not None:
+        from .bricks import model_handle
+
+        mh = model_handle(model)
+        N.check(N.lib().xb_sample_scan(mh.h, int(field), len(pts), N.ptr(pts), N.ptr(out)))
+    else:
+        if not 0 <= field < cells.n_fields:
+            raise ValueError(f"field {field} out of range for {cells.n_fields} fields")
+        dev = N.require_device()
+        h = N.new_handle()
+        n = len(cells)
+        N.check(N.lib().xb_cells_create(n, dev, C.byref(h)))
+        ch = N.CellsHandle(h.value, dev)
+        arrs = [np.ascontiguousarray(a, np.int32) for a in (cells.i, cells.j, cells.k, cells.level)]
+        arrs.append(np.ascontiguousarray(cells.values[:, field], np.float32))
+        N.check(N.lib().xb_cells_upload(ch.h, 0, n, *(N.ptr(x) for x in arrs)))
+        N.check(N.lib().xb_sample_scan_cells(ch.h, len(pts), N.ptr(pts), N.ptr(out)))
     num, den = out[0]
     return SampleResult(num / den, den, True) if den > EPS_WEIGHT else SampleResult(0.0, den, False)
 

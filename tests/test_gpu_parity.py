@@ -152,6 +152,42 @@ def test_oracle_scan_matches_golden_outside(xb, name):
         assert (s.value, s.weight_sum, s.valid) == (g["pts_value"][t], g["pts_wsum"][t], bool(g["pts_valid"][t]))
 
 
+def _scan_cells_py(cells, p):
+    """_accumulate_cells (R/sampling.py:106-120) in plain Python floats (IEEE double, no FMA)."""
+    w = np.exp2(cells.level.astype(np.float64))
+    hx = 1.0 - np.abs((cells.i + 0.5 * w) - p[0]) / w
+    hy = 1.0 - np.abs((cells.j + 0.5 * w) - p[1]) / w
+    hz = 1.0 - np.abs((cells.k + 0.5 * w) - p[2]) / w
+    num = den = 0.0
+    for t in np.nonzero((hx > 0) & (hy > 0) & (hz > 0))[0]:  # list order
+        h = float(hx[t]) * float(hy[t]) * float(hz[t])
+        num += h * float(cells.values[t, 0])
+        den += h
+    return num, den
+
+
+@pytest.mark.parametrize("name", ["gauss16", "mixed_levels"])
+def test_oracle_scan_of_plain_cell_lists(xb, name):
+    """basis_sample_oracle on a CellList that is not a model's canonical list (generator
+    order, and shuffled): scanned in its own order like the reference (R/sampling.py:291-298)."""
+    from paper_2009_03076_b200.model import CellList
+    from paper_2009_03076_b200.sampling import EPS_WEIGHT, basis_sample_oracle
+
+    g = golden_model(name)
+    c0 = _cells(name)
+    perm = np.random.default_rng(3).permutation(len(c0))
+    c1 = CellList(c0.i[perm], c0.j[perm], c0.k[perm], c0.level[perm], c0.values[perm])
+    for cl in (c0, c1):
+        for t in range(0, len(g["pts"]), max(1, len(g["pts"]) // 25)):
+            p = g["pts"][t]
+            num, den = _scan_cells_py(cl, p)
+            s = basis_sample_oracle(p, cl)
+            assert s.weight_sum == den
+            assert s.valid == (den > EPS_WEIGHT)
+            if s.valid:
+                assert s.value == num / den
+
+
 # ---------------------------------------------------------------- traversal
 
 
@@ -516,3 +552,24 @@ def test_tiled_ranks_reassemble_the_frame(xb, world):
     torch.cuda.synchronize()
     assert np.array_equal(img.cpu().numpy(), full.rgba)
     assert tuple(tot) == (full.stats.regions, full.stats.samples)
+
+
+def test_large_frames_render_in_bands(xb):
+    """Frames above 4M pixels run as interleaved tile bands (bounded walk scratch):
+    pixel-identical to the single-pass float path, same counters."""
+    from paper_2009_03076_b200.accel import TransferFunction
+    from paper_2009_03076_b200.orbit import orbit_cameras
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame, render_frame_float
+
+    model, _, regions = _build("smoke")
+    lo, hi = model.value_range(0)
+    tf = TransferFunction.grayscale((lo, hi), max_alpha=0.5)
+    scene = build_scene(model, regions, tf)
+    cam = orbit_cameras(regions.bounds, 3, 2304, 2048)[1]  # 4.7M px -> 2 bands
+    params = MarchParams(seed=2, gradient_mode="analytic")
+    fr = render_frame(scene, cam, tf, params)
+    u8, f64, cnt, st = render_frame_float(scene, cam, tf, params)
+    assert np.array_equal(fr.rgba, u8)
+    assert (fr.stats.regions, fr.stats.samples) == (int(st[0]), int(st[1])) == (int(cnt[..., 0].sum()),
+                                                                               int(cnt[..., 1].sum()))
+    assert fr.stats.samples > 0
