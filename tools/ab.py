@@ -24,7 +24,7 @@ model, _ = build_bricks(cells)
 regions = build_regions(model)
 tf = bench.tf_for(model.value_range(0), cfg)
 scene = build_scene(model, regions, tf, iso_value=cfg.get("iso"))
-cam = bench.camera_for(regions.bounds, cfg, 0)
+cam = bench.cameras_for(regions.bounds, cfg, 8)[int(os.environ.get('AB_VIEW', '0'))]
 params = MarchParaNAMED = {"warp": {}, "tile": {"kernel": 1}, "lbvh": {"traversal": 1}, "nowalk": {"walk_lists": 0},
          "short": {"short_rays": 1}, "noshort": {"short_rays": 0}, "kshort": {"short_rays": 1, "fuse_short": 0}}
 
@@ -39,6 +39,8 @@ def setv(v):
     from paper_2009_03076_b200 import _native as N
     import ctypes as C
 
+    if not hasattr(N.lib(), "xb_tuning_set"):  # round-1 build: defaults only
+        return
     t = N.XbTuning()
     N.lib().xb_tuning_defaults(C.byref(t))
     for k, val in fields_of(v).items():

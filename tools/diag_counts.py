@@ -17,7 +17,7 @@ model, _ = build_bricks(cells)
 regions = build_regions(model)
 tf = bench.tf_for(model.value_range(0), cfg)
 scene = build_scene(model, regions, tf)
-cam = bench.camera_for(regions.bounds, cfg, 0)
+cam = bench.cameras_for(regions.bounds, cfg, 8)[0]
 params = MarchParams(seed=0, gradient_mode=cfg["gradient"])
 for i in range(3):
     fr = render_frame(scene, cam, tf, params)

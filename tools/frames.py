@@ -23,7 +23,7 @@ model, _ = build_bricks(cells)
 regions = build_regions(model)
 tf = bench.tf_for(model.value_range(0), cfg)
 scene = build_scene(model, regions, tf, iso_value=cfg.get("iso"))
-cam = bench.camera_for(regions.bounds, cfg, view)
+cam = bench.cameras_for(regions.bounds, cfg, 8)[view]
 params = MarchParams(seed=0, gradient_mode=cfg["gradient"])
 W, H = cfg["res"]
 out = torch.empty((H, W, 4), dtype=torch.uint8, device="cuda")

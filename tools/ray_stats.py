@@ -18,7 +18,7 @@ regions = build_regions(model)
 del cells
 tf = bench.tf_for(model.value_range(0), cfg)
 scene = R.build_scene(model, regions, tf, iso_value=cfg.get("iso"))
-cam = bench.camera_for(regions.bounds, cfg, 0)
+cam = bench.cameras_for(regions.bounds, cfg, 8)[0]
 params = R.MarchParams(seed=0, gradient_mode=cfg["gradient"])
 _, _, cnt, st = R.render_frame_float(scene, cam, tf, params)
 reg, smp = cnt[..., 0].ravel().astype(np.int64), cnt[..., 1].ravel().astype(np.int64)
