@@ -168,6 +168,18 @@ def make_cells(cfg, host=False):
     if cfg.get("gpu_gen"):
         dc = xio.generate_synthetic_device(spec)
         return dc.to_host() if host else dc
+    cache = os.environ.get("XB_CELL_CACHE")  # tools/ab.py: reuse one generation across A/B processes
+    if cache:
+        from paper_2009_03076_b200.model import CellList
+
+        key = Path(cache) / (hashlib.sha256(repr(spec).encode()).hexdigest()[:16] + ".npz")
+        if key.exists():
+            z = np.load(key)
+            return CellList(z["i"], z["j"], z["k"], z["level"], z["values"], (spec.field_name,))
+        cl = xio.generate_synthetic(spec, workers=os.cpu_count() or 1)
+        key.parent.mkdir(parents=True, exist_ok=True)
+        np.savez(key, i=cl.i, j=cl.j, k=cl.k, level=cl.level, values=cl.values)
+        return cl
     return xio.generate_synthetic(spec, workers=os.cpu_count() or 1)
 
 
