@@ -592,29 +592,26 @@ __device__ __forceinline__ RbRec load_rb(const RbRec* __restrict__ p) {
 }
 
 // Running state of the frame gather of one sample (value sums in the
-// reference's exact FP64 sequence; FP32 shading-gradient partials kept as
-// (dz = 0, dz = 1) pairs for the f32x2 instructions of sm_100 — the pair is
-// summed once per sample).
+// reference's exact FP64 sequence; FP32 shading-gradient partials).  Pairing
+// the FP32 partials over dz on sm_100's f32x2 instructions cut brick_step from
+// 258 to 239 SASS instructions but measured slower (orbit-mean C3 0.904 vs
+// 0.897 ms, C2 6.17 vs 6.04: longer dependent chains, 40 more spill bytes).
 struct ShadeAcc {
     double num, den;
-    float2 gnum, dn0, dn1, dn2;  // per-dz partials of sum h u, sum (dh/dx) u, ...
-    float2 fd0, dd12;            // (sum h, sum dh/dx), (sum dh/dy, sum dh/dz)
-    float v0;
+    float fden, gnum, dn0, dn1, dn2, dd0, dd1, dd2, v0;
     int n_nz;
     bool have_ref;
     __device__ __forceinline__ void clear() {
         num = den = 0.0;
-        gnum = dn0 = dn1 = dn2 = fd0 = dd12 = make_float2(0.f, 0.f);
-        v0 = 0.f;
+        fden = gnum = dn0 = dn1 = dn2 = dd0 = dd1 = dd2 = v0 = 0.f;
         n_nz = 0;
         have_ref = false;
     }
     // quotient-rule numerator of the analytic gradient (direction only, see FastAccum)
     __device__ __forceinline__ void gradient(float g[3]) const {
-        const float gn = gnum.x + gnum.y, fden = fd0.x;
-        g[0] = (dn0.x + dn0.y) * fden - gn * fd0.y;
-        g[1] = (dn1.x + dn1.y) * fden - gn * dd12.x;
-        g[2] = (dn2.x + dn2.y) * fden - gn * dd12.y;
+        g[0] = dn0 * fden - gnum * dd0;
+        g[1] = dn1 * fden - gnum * dd1;
+        g[2] = dn2 * fden - gnum * dd2;
     }
 };
 
@@ -708,39 +705,29 @@ __device__ __forceinline__ void brick_step(const SceneView& S, const RbRec& B, d
             A.v0 = Z.v0 ? p0 : p1;  // select chain: no local-memory indexing
             A.have_ref = true;
         }
-        // FP32 gradient partials with paired (dz = 0, 1) f32x2 operations:
-        //   A_dy = sum_x hx u, B_dy = sum_x sx u          (per row dy, both dz at once)
-        //   C = sum_y hy A, D = sum_y hy B, E = sum_y sy A (both dz)
-        //   gnum += hz C, dn_x += hz D, dn_y += hz E, dn_z += sz C   (per-dz pairs kept)
         const float ax0 = (float)X.h0, ax1 = (float)X.h1, ay0 = (float)Y.h0, ay1 = (float)Y.h1,
                     az0 = (float)Z.h0, az1 = (float)Z.h1;
-        const float2 V0 = make_float2(A.v0, A.v0);
-        const float2 u00 = __fadd2_rn(make_float2(vv[0][0][0], vv[1][0][0]), make_float2(-A.v0, -A.v0));
-        const float2 u01 = __fadd2_rn(make_float2(vv[0][0][1], vv[1][0][1]), make_float2(-A.v0, -A.v0));
-        const float2 u10 = __fadd2_rn(make_float2(vv[0][1][0], vv[1][1][0]), make_float2(-A.v0, -A.v0));
-        const float2 u11 = __fadd2_rn(make_float2(vv[0][1][1], vv[1][1][1]), make_float2(-A.v0, -A.v0));
-        (void)V0;
-        const float2 hx0 = make_float2(ax0, ax0), hx1 = make_float2(ax1, ax1);
-        const float2 sx0 = make_float2(X.s0, X.s0), sx1 = make_float2(X.s1, X.s1);
-        const float2 A0 = __ffma2_rn(hx1, u01, __fmul2_rn(hx0, u00)), A1 = __ffma2_rn(hx1, u11, __fmul2_rn(hx0, u10));
-        const float2 B0 = __ffma2_rn(sx1, u01, __fmul2_rn(sx0, u00)), B1 = __ffma2_rn(sx1, u11, __fmul2_rn(sx0, u10));
-        const float2 hy0 = make_float2(ay0, ay0), hy1 = make_float2(ay1, ay1);
-        const float2 sy0 = make_float2(Y.s0, Y.s0), sy1 = make_float2(Y.s1, Y.s1);
-        const float2 C = __ffma2_rn(hy1, A1, __fmul2_rn(hy0, A0));
-        const float2 D = __ffma2_rn(hy1, B1, __fmul2_rn(hy0, B0));
-        const float2 E = __ffma2_rn(sy1, A1, __fmul2_rn(sy0, A0));
-        const float2 hz = make_float2(az0, az1), sz = make_float2(Z.s0, Z.s1);
-        A.gnum = __ffma2_rn(hz, C, A.gnum);
-        A.dn0 = __ffma2_rn(hz, D, A.dn0);
-        A.dn1 = __ffma2_rn(hz, E, A.dn1);
-        A.dn2 = __ffma2_rn(sz, C, A.dn2);
-        // den and its derivatives, separable: (Hx, Sx) * Hy Hz and Hx * (Sy Hz, Hy Sz)
-        const float2 HS_x = __fadd2_rn(make_float2(ax0, X.s0), make_float2(ax1, X.s1));
-        const float2 SH_y = __fadd2_rn(make_float2(Y.s0, ay0), make_float2(Y.s1, ay1));
-        const float2 HS_z = __fadd2_rn(make_float2(az0, Z.s0), make_float2(az1, Z.s1));
-        const float Hyz = (ay0 + ay1) * HS_z.x;
-        A.fd0 = __ffma2_rn(HS_x, make_float2(Hyz, Hyz), A.fd0);
-        A.dd12 = __ffma2_rn(make_float2(HS_x.x, HS_x.x), __fmul2_rn(SH_y, HS_z), A.dd12);
+        float C[2], D[2], E[2];
+#pragma unroll
+        for (int dz = 0; dz < 2; dz++) {
+            const float u00 = vv[dz][0][0] - A.v0, u01 = vv[dz][0][1] - A.v0;
+            const float u10 = vv[dz][1][0] - A.v0, u11 = vv[dz][1][1] - A.v0;
+            const float A0 = fmaf(ax1, u01, ax0 * u00), A1 = fmaf(ax1, u11, ax0 * u10);      // x-hat reductions
+            const float B0 = fmaf(X.s1, u01, X.s0 * u00), B1 = fmaf(X.s1, u11, X.s0 * u10);  // x-slope reductions
+            C[dz] = fmaf(ay1, A1, ay0 * A0);  // sum hx hy u
+            D[dz] = fmaf(ay1, B1, ay0 * B0);  // sum sx hy u
+            E[dz] = fmaf(Y.s1, A1, Y.s0 * A0);  // sum hx sy u
+        }
+        A.gnum = fmaf(az1, C[1], fmaf(az0, C[0], A.gnum));
+        A.dn0 = fmaf(az1, D[1], fmaf(az0, D[0], A.dn0));
+        A.dn1 = fmaf(az1, E[1], fmaf(az0, E[0], A.dn1));
+        A.dn2 = fmaf(Z.s1, C[1], fmaf(Z.s0, C[0], A.dn2));
+        const float Hx = ax0 + ax1, Hy = ay0 + ay1, Hz = az0 + az1;
+        const float Sx = X.s0 + X.s1, Sy = Y.s0 + Y.s1, Sz = Z.s0 + Z.s1;
+        A.fden = fmaf(Hx * Hy, Hz, A.fden);
+        A.dd0 = fmaf(Sx * Hy, Hz, A.dd0);
+        A.dd1 = fmaf(Hx * Sy, Hz, A.dd1);
+        A.dd2 = fmaf(Hx * Hy, Sz, A.dd2);
     }
 }
 
