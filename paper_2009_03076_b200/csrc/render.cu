@@ -1053,9 +1053,12 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         {
                             ShadeAcc G;
                             G.clear();
+                            // one convergent loop: owner lanes take [0, half) (all of it when not
+                            // helped), helper lanes [half, nids), idle lanes nothing
                             const int half = (nids + 1) >> 1;
-                            if (act) gather_acc<GRAD == 1>(S, (int64_t)sq.ids, helped ? half : nids, px, py, pz, G);
-                            else if (helper) gather_acc<GRAD == 1>(S, (int64_t)sq.ids + half, nids - half, px, py, pz, G);
+                            const int g_beg = helper ? half : 0;
+                            const int g_cnt = act ? (helped ? half : nids) : (helper ? nids - half : 0);
+                            gather_acc<GRAD == 1>(S, (int64_t)sq.ids + g_beg, g_cnt, px, py, pz, G);
                             if (kHelpers && m < 32) {  // warp-uniform: fetch the helper's partials (lane + m)
                                 const int src = (lane + m) & 31;
                                 const double hn = __shfl_sync(FULL, G.num, src), hd = __shfl_sync(FULL, G.den, src);
