@@ -731,51 +731,18 @@ __device__ __forceinline__ void brick_step(const SceneView& S, const RbRec& B, d
     }
 }
 
-// the frame gather over region-list entries [off, off + nids) (S.rb), into A
-template <bool GRAD>
-__device__ __forceinline__ void gather_acc(const SceneView& S, int64_t off, int nids, double px, double py, double pz,
-                                           ShadeAcc& A) {
-    const RbRec* __restrict__ rb = S.rb + off;
-    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, load_rb(rb + t), px, py, pz, A);
-}
-
-__device__ __forceinline__ void finish_gather(const ShadeAcc& A, bool grad, FastAccum& F) {
-    F.num = A.num;
-    F.den = A.den;
-    F.n_nz = A.n_nz;
-    if (grad) A.gradient(F.g);
-}
-
+// the frame gather over region-list entries [off, off + nids) (S.rb)
 template <bool GRAD>
 __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, int nids, double px, double py,
                                              double pz, FastAccum& F) {
     ShadeAcc A;
     A.clear();
-    gather_acc<GRAD>(S, off, nids, px, py, pz, A);
-    finish_gather(A, GRAD, F);
-}
-
-// Adds the partials of the later part of a brick list (B, gathered from zero
-// by a helper lane) to those of the earlier part (A).  The value sums are
-// reassociated at the split (within an ulp); the gradient partials of B are
-// re-referenced from its first contributing value to A's:
-// sum h (v - v0a) = sum h (v - v0b) + (v0b - v0a) sum h, likewise for the slopes.
-__device__ __forceinline__ void merge_later(ShadeAcc& A, double num, double den, int n_nz, bool have, float v0,
-                                            float gnum, float dn0, float dn1, float dn2, float fden, float dd0,
-                                            float dd1, float dd2) {
-    A.num += num;
-    A.den += den;
-    A.n_nz += n_nz;
-    if (!have) return;
-    float sh = 0.f;
-    if (A.have_ref) sh = v0 - A.v0;
-    else { A.v0 = v0; A.have_ref = true; }
-    A.gnum += fmaf(sh, fden, gnum);
-    A.dn0 += fmaf(sh, dd0, dn0);
-    A.dn1 += fmaf(sh, dd1, dn1);
-    A.dn2 += fmaf(sh, dd2, dn2);
-    A.fden += fden;
-    A.dd0 += dd0; A.dd1 += dd1; A.dd2 += dd2;
+    const RbRec* __restrict__ rb = S.rb + off;
+    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, load_rb(rb + t), px, py, pz, A);
+    F.num = A.num;
+    F.den = A.den;
+    F.n_nz = A.n_nz;
+    if (GRAD) A.gradient(F.g);
 }
 
 // _shade_factor (R/render.py:284-289) on an unnormalised FP32 gradient direction

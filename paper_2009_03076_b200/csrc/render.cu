@@ -139,18 +139,17 @@ constexpr int kWarpThreads = 128;
 #endif
 constexpr int kWarpMinBlocks = XB_WARP_MINB;
 constexpr int kWarpsPerBlock = kWarpThreads / 32;
-// partial chunks lend their idle lanes to the first samples' brick lists (see the chunk gather)
-#ifndef XB_HELPERS
-#define XB_HELPERS 1
-#endif
-constexpr bool kHelpers = XB_HELPERS != 0;
 constexpr int kWarpStack = 256;  // spilled frontier entries per warp
 constexpr int kRaysPerGrab = 8;  // rays taken per work-counter atomic
 // A (sample, brick)-flattened chunk gather (each lane one brick per round,
 // partials combined through shared memory) measured slower every time — C2
 // 12.3 vs 10.1 ms (first pipeline), C3 1.21 vs 0.92 and C2 8.74 vs 6.31 (walk
 // lists): the per-round barriers and the combine loop cost more than the idle
-// lane-brick slots of the per-sample loop.  Removed in round 2.
+// lane-brick slots of the per-sample loop.  Removed in round 2.  Round 2 also
+// measured "helper lanes" — a partial chunk's idle lane m + j gathering the
+// later half of sample j's brick list, merged by shuffles (one convergent
+// loop): orbit-mean C3 0.927 vs 0.897 ms, C2 6.40 vs 6.04 — slower as well
+// (the merge state and shuffles cost more than the idle lanes).
 
 struct SegQ {       // one visited region of the segment queue
     double ci, co;   // clipped interval
@@ -1006,13 +1005,8 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             atomicAdd(A.dbg, 1ull);
                             atomicAdd(A.dbg + 1, (unsigned long long)m);
                         }
-                        // helper lanes: in a partial chunk, idle lane m + j gathers the later half
-                        // of sample j's brick list (j < 32 - m), merged into lane j after the gather
-                        const bool helper = kHelpers && lane >= m && lane - m < m;
-                        const bool helped = kHelpers && lane < m && lane + m < 32;
-                        const int s = h0 + (helper ? lane - m : lane);
+                        const int s = h0 + lane;
                         const bool act = lane < m;
-                        const bool work = act || helper;
                         int sg = 0;  // segment of sample s: #{i : q_P[i] <= s}
 #pragma unroll
                         for (int b = 16; b >= 1; b >>= 1) {
@@ -1027,7 +1021,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         const int lev = sq.meta >> 24;
                         const int nids = sq.meta & 0xffffff;
                         double sl = 0.0, px = 0.0, py = 0.0, pz = 0.0;
-                        if (work) {
+                        if (act) {
                             const double s_dt = A.M.lv_dt[lev];
                             const int j = s - (s_end - sq.cnt);
                             const double prev = j == 0 ? sq.ci : s_dt * ((sq.kf + (double)(j - 1)) + rho);
@@ -1050,34 +1044,8 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             }
                         }
                         FastAccum F;
-                        {
-                            ShadeAcc G;
-                            G.clear();
-                            // one convergent loop: owner lanes take [0, half) (all of it when not
-                            // helped), helper lanes [half, nids), idle lanes nothing
-                            const int half = (nids + 1) >> 1;
-                            const int g_beg = helper ? half : 0;
-                            const int g_cnt = act ? (helped ? half : nids) : (helper ? nids - half : 0);
-                            gather_acc<GRAD == 1>(S, (int64_t)sq.ids + g_beg, g_cnt, px, py, pz, G);
-                            if (kHelpers && m < 32) {  // warp-uniform: fetch the helper's partials (lane + m)
-                                const int src = (lane + m) & 31;
-                                const double hn = __shfl_sync(FULL, G.num, src), hd = __shfl_sync(FULL, G.den, src);
-                                const int hz = __shfl_sync(FULL, G.n_nz, src);
-                                if (GRAD == 1) {
-                                    const bool hv = __shfl_sync(FULL, (int)G.have_ref, src) != 0;
-                                    const float v0 = __shfl_sync(FULL, G.v0, src), gn = __shfl_sync(FULL, G.gnum, src);
-                                    const float d0 = __shfl_sync(FULL, G.dn0, src), d1 = __shfl_sync(FULL, G.dn1, src),
-                                                d2 = __shfl_sync(FULL, G.dn2, src), fd = __shfl_sync(FULL, G.fden, src);
-                                    const float e0 = __shfl_sync(FULL, G.dd0, src), e1 = __shfl_sync(FULL, G.dd1, src),
-                                                e2 = __shfl_sync(FULL, G.dd2, src);
-                                    if (helped) merge_later(G, hn, hd, hz, hv, v0, gn, d0, d1, d2, fd, e0, e1, e2);
-                                } else if (helped) {
-                                    G.num += hn;
-                                    G.den += hd;
-                                    G.n_nz += hz;
-                                }
-                            }
-                            finish_gather(G, GRAD == 1, F);
+                        if (act) {
+                            gather_shade<GRAD == 1>(S, (int64_t)sq.ids, nids, px, py, pz, F);
                         }
                         if (act) {
                             if (COUNT) my_bytes = 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
