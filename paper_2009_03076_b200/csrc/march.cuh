@@ -23,6 +23,9 @@ namespace xb {
 
 constexpr double kEpsWeight = 1e-12;     // EPS_WEIGHT, R/sampling.py:37
 
+#ifndef XB_GATHER_VARIANT
+#define XB_GATHER_VARIANT 0
+#endif
 #ifndef XB_INT_TESTS
 #define XB_INT_TESTS 1
 #endif
@@ -738,7 +741,20 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, in
     ShadeAcc A;
     A.clear();
     const RbRec* __restrict__ rb = S.rb + off;
+#if XB_GATHER_VARIANT == 1
+#pragma unroll 2
     for (int t = 0; t < nids; t++) brick_step<GRAD>(S, load_rb(rb + t), px, py, pz, A);
+#elif XB_GATHER_VARIANT == 2
+    // software pipeline: the next brick record is in flight while this brick runs
+    RbRec cur = load_rb(rb);
+    for (int t = 0; t < nids; t++) {
+        const RbRec nxt = load_rb(rb + min(t + 1, nids - 1));
+        brick_step<GRAD>(S, cur, px, py, pz, A);
+        cur = nxt;
+    }
+#else
+    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, load_rb(rb + t), px, py, pz, A);
+#endif
     F.num = A.num;
     F.den = A.den;
     F.n_nz = A.n_nz;
