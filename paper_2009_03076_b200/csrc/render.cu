@@ -1,8 +1,8 @@
 // render.cu — the fused sm_100a ray-march kernels (paper §4-5) and the
 // single-ray batch kernel behind integrate_ray / iso_intersect.
 //
-// Frame pipeline: k_classify -> CUB hit select -> k_walkp<1> ->
-// k_route -> k_walkp<2> -> k_warp (warp per long ray, then a lane per short
+// Frame pipeline: k_classify -> CUB hit select -> k_walk ->
+// k_route -> k_walk2 -> k_warp (warp per long ray, then a lane per short
 // ray); iso scenes run the same chain on the iso set first, ending in
 // k_iso_warp.  k_render: one thread per pixel, one block per tile — the
 // kernel of the per-visit LBVH traversal and the cell-location gather
@@ -323,118 +323,106 @@ __global__ void __launch_bounds__(kWalkThreads) k_classify(const __grid_constant
 // The walk itself (front to back over the Kd4 tree from `code` with the
 // ordered stack st_*[0, sp_n)), listing leaves into out[count..cap); on a stop
 // it sets `flags` and saves the ordered remainder for k_warp.
-// State of one ray's ordered walk (k_walkp<1> / <2>, one lane each).
-struct WalkLane {
-    int code;        // current entry: Kd4 node >= 0, leaf region -2 - id, kNoEntry
-    double tn, tf;   // its interval
-    int sp_n;        // stack depth
-    int count;       // leaves listed
-    int flags;       // kLeafTruncated | kLeafTauStop | kLeafHeavy
-    float est, tau;  // estimated samples (short-ray test), opacity minorant depth
-};
-
-// One step of a ray's walk: list a leaf, or expand a Kd4 node (nearest child
-// next, the others stacked farthest-first), or pop.  Returns false when the
-// walk is over (list complete, cap reached, or the opacity minorant passed
-// tau_stop: the ordered remainder is saved for k_warp / k_walk2).
-__device__ __forceinline__ bool walk_step(const RenderArgs& A, int64_t slot, const Ray& r, const int sg[3],
-                                          double tmin, double tmax, WalkLane& W, int* st_code, float* st_tn,
-                                          float* st_tf, int32_t* __restrict__ out, int cap) {
+__device__ __forceinline__ void walk_leaves(const RenderArgs& A, int64_t slot, const Ray& r, const int sg[3],
+                                            double tmin, double tmax, int code, double tn, double tf, int* st_code,
+                                            float* st_tn, float* st_tf, int sp_n, int32_t* __restrict__ out,
+                                            int& count, int& flags, int cap, float& est) {
     const SceneView& S = A.S;
-    if (W.code <= -2) {  // a leaf: list it
-        if (W.count == cap) {  // resume from this leaf
-            W.flags = kLeafTruncated;
-            save_resume(A, slot, W.code, W.tn, W.tf, st_code, st_tn, st_tf, W.sp_n);
-            return false;
-        }
-        const int rid = -2 - W.code;
-        out[W.count++] = rid;
-        if (A.short_list && W.count <= A.short_leaves && W.est <= A.short_samples)  // samples ~ len/dt + 1
-            W.est += (float)((W.tf - W.tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
-        if (A.wqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
-            W.tau += __ldg(A.wqmin + rid) * (float)(W.tf - W.tn) * (float)A.M.spc;
-            if (W.tau > A.walk_tau_stop) {
-                W.flags = kLeafTruncated | kLeafTauStop;
-                save_resume(A, slot, kNoEntry, 0.0, 0.0, st_code, st_tn, st_tf, W.sp_n);
-                return false;
+    const float spc = (float)A.M.spc, tau_stop = A.walk_tau_stop;
+    float tau = 0.f;
+    for (;;) {
+        if (code <= -2) {  // a leaf: list it
+            if (count == cap) {  // resume from this leaf
+                flags = kLeafTruncated;
+                save_resume(A, slot, code, tn, tf, st_code, st_tn, st_tf, sp_n);
+                break;
             }
-        }
-    } else {
-        // expand the Kd4 node (same classification as kd_next / k_warp)
-        const int code = W.code;
-        const double tn = W.tn, tf = W.tf;
-        const Kd4Node nd = S.kd4[code];
-        const uint32_t msk = A.wmask4[code];
-        int oc[4];
-        double olo[4], ohi[4];
-        int no = 0;
-        int hs0 = 0, hs1 = 0, nh = 1;
-        double hn0 = tn, hf0 = tf, hn1 = 0.0, hf1 = 0.0;
-        {
-            const int ax = nd.axes & 3;
-            const double p = (double)nd.plane[0] * 0.5;
-            const double oa = sel3(ax, r.o);
-            const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
-            if (sa == 0) {
-                hs0 = oa < p ? 0 : 1;
-            } else {
-                const double tp = (p - oa) * sel3(ax, r.inv);
-                const int ns_ = sa > 0 ? 0 : 1;
-                if (tp >= tf) hs0 = ns_;
-                else if (tp <= tn) hs0 = 1 - ns_;
-                else { hs0 = ns_; hf0 = tp; hs1 = 1 - ns_; hn1 = tp; hf1 = tf; nh = 2; }
+            const int rid = -2 - code;
+            out[count++] = rid;
+            if (A.short_list && count <= A.short_leaves && est <= A.short_samples)  // samples ~ len/dt + 1
+                est += (float)((tf - tn) / A.M.lv_dt[S.rec[rid].meta >> 24]) + 1.f;
+            if (A.wqmin) {  // early-stop heuristic: opacity surely past `early` (k_warp verifies)
+                tau += __ldg(A.wqmin + rid) * (float)(tf - tn) * spc;
+                if (tau > tau_stop) {
+                    flags = kLeafTruncated | kLeafTauStop;
+                    save_resume(A, slot, kNoEntry, 0.0, 0.0, st_code, st_tn, st_tf, sp_n);
+                    break;
+                }
             }
-        }
+        } else {
+            // expand the Kd4 node (same classification as kd_next / k_warp)
+            const Kd4Node nd = S.kd4[code];
+            const uint32_t msk = A.wmask4[code];
+            int oc[4];
+            double olo[4], ohi[4];
+            int no = 0;
+            int hs0 = 0, hs1 = 0, nh = 1;
+            double hn0 = tn, hf0 = tf, hn1 = 0.0, hf1 = 0.0;
+            {
+                const int ax = nd.axes & 3;
+                const double p = (double)nd.plane[0] * 0.5;
+                const double oa = sel3(ax, r.o);
+                const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
+                if (sa == 0) {
+                    hs0 = oa < p ? 0 : 1;
+                } else {
+                    const double tp = (p - oa) * sel3(ax, r.inv);
+                    const int ns_ = sa > 0 ? 0 : 1;
+                    if (tp >= tf) hs0 = ns_;
+                    else if (tp <= tn) hs0 = 1 - ns_;
+                    else { hs0 = ns_; hf0 = tp; hs1 = 1 - ns_; hn1 = tp; hf1 = tf; nh = 2; }
+                }
+            }
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            if (h < nh) {
-                const int sd = h ? hs1 : hs0;
-                const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
-                const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
-                int s0 = 2 * sd, s1 = -1;
-                double a0 = hn, b0 = hf, a1 = 0.0, b1 = 0.0;
-                if (ax != 3) {
-                    const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
-                    const double oa = sel3(ax, r.o);
-                    const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
-                    if (sa == 0) {
-                        s0 = 2 * sd + (oa < p ? 0 : 1);
-                    } else {
-                        const double tp = (p - oa) * sel3(ax, r.inv);
-                        const int nq = sa > 0 ? 0 : 1;
-                        if (tp >= b0) s0 = 2 * sd + nq;
-                        else if (tp <= a0) s0 = 2 * sd + 1 - nq;
-                        else { s0 = 2 * sd + nq; b0 = tp; s1 = 2 * sd + 1 - nq; a1 = tp; b1 = hf; }
+            for (int h = 0; h < 2; h++) {
+                if (h < nh) {
+                    const int sd = h ? hs1 : hs0;
+                    const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
+                    const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
+                    int s0 = 2 * sd, s1 = -1;
+                    double a0 = hn, b0 = hf, a1 = 0.0, b1 = 0.0;
+                    if (ax != 3) {
+                        const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
+                        const double oa = sel3(ax, r.o);
+                        const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
+                        if (sa == 0) {
+                            s0 = 2 * sd + (oa < p ? 0 : 1);
+                        } else {
+                            const double tp = (p - oa) * sel3(ax, r.inv);
+                            const int nq = sa > 0 ? 0 : 1;
+                            if (tp >= b0) s0 = 2 * sd + nq;
+                            else if (tp <= a0) s0 = 2 * sd + 1 - nq;
+                            else { s0 = 2 * sd + nq; b0 = tp; s1 = 2 * sd + 1 - nq; a1 = tp; b1 = hf; }
+                        }
+                    }
+                    if (((msk >> s0) & 1) && b0 > tmin && a0 < tmax) {
+                        oc[no] = kd4_child(nd, s0); olo[no] = a0; ohi[no] = b0; no++;
+                    }
+                    if (s1 >= 0 && ((msk >> s1) & 1) && b1 > tmin && a1 < tmax) {
+                        oc[no] = kd4_child(nd, s1); olo[no] = a1; ohi[no] = b1; no++;
                     }
                 }
-                if (((msk >> s0) & 1) && b0 > tmin && a0 < tmax) {
-                    oc[no] = kd4_child(nd, s0); olo[no] = a0; ohi[no] = b0; no++;
+            }
+            if (no > 0) {  // continue with the nearest child, stack the others farthest-first
+                if (sp_n + no - 1 > kWalkStack) __trap();  // depth-bounded: <= 3 per Kd4 level
+                for (int c = no - 1; c >= 1; c--) {
+                    st_code[sp_n] = oc[c];
+                    st_tn[sp_n] = __double2float_rd(olo[c]);
+                    st_tf[sp_n] = __double2float_ru(ohi[c]);
+                    sp_n++;
                 }
-                if (s1 >= 0 && ((msk >> s1) & 1) && b1 > tmin && a1 < tmax) {
-                    oc[no] = kd4_child(nd, s1); olo[no] = a1; ohi[no] = b1; no++;
-                }
+                code = oc[0];
+                tn = olo[0];
+                tf = ohi[0];
+                continue;
             }
         }
-        if (no > 0) {  // continue with the nearest child, stack the others farthest-first
-            if (W.sp_n + no - 1 > kWalkStack) __trap();  // depth-bounded: <= 3 per Kd4 level
-            for (int c = no - 1; c >= 1; c--) {
-                st_code[W.sp_n] = oc[c];
-                st_tn[W.sp_n] = __double2float_rd(olo[c]);
-                st_tf[W.sp_n] = __double2float_ru(ohi[c]);
-                W.sp_n++;
-            }
-            W.code = oc[0];
-            W.tn = olo[0];
-            W.tf = ohi[0];
-            return true;
-        }
+        if (sp_n == 0) break;
+        --sp_n;
+        code = st_code[sp_n];
+        tn = (double)st_tn[sp_n];
+        tf = (double)st_tf[sp_n];
     }
-    if (W.sp_n == 0) return false;
-    --W.sp_n;
-    W.code = st_code[W.sp_n];
-    W.tn = (double)st_tn[W.sp_n];
-    W.tf = (double)st_tf[W.sp_n];
-    return true;
 }
 
 // route of a walked ray: short (complete list of <= short_leaves leaves, few
@@ -447,121 +435,56 @@ __device__ __forceinline__ void route_of(const RenderArgs& A, int v, bool& is_sh
     is_cut = A.cut_list && (v & kLeafTruncated) && (A.cut_tau || !(v & kLeafTauStop));
 }
 
-
-// Persistent walks with lane refill (k_walkp<1> = pass 1 over the hit list,
-// k_walkp<2> = pass 2 over the cut list): every lane runs its own ray's walk
-// one step at a time and takes the next ray as soon as its walk ends (one
-// warp-aggregated atomic per refill), so a warp no longer waits for its
-// longest walk — one ray per thread for a whole block left 10-15 of 32 lanes
-// active in C2's walks (ncu).  Results are per slot and identical to the
-// one-ray-per-thread kernels (same walk_step sequence).
-template <int PASS>
-__device__ __forceinline__ bool walk_begin(const RenderArgs& A, int64_t ci, int64_t& slot, SlotPix& spx, Ray& r,
-                                           int sg[3], double& tmin, double& tmax, WalkLane& W, int* st_code,
-                                           float* st_tn, float* st_tf) {
+__global__ void __launch_bounds__(kWalkThreads) k_walk(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const SceneView& S = A.S;
-    slot = PASS == 1 ? A.hit_list[ci] : A.cut_list[ci];
-    spx = slot_pixel(A, slot);
-    if (PASS == 2) {
-        const int32_t* res = A.resume + slot * (int64_t)(1 + 3 * kResume);
-        const int m = res[0];
-        if (m <= 0) return false;  // remainder not saved: k_warp restarts at the root
-        pixel_ray(A, spx.x, spx.y, r);
-        tmin = 0.0;
-        tmax = kTFar;
-        clip_ray(A.M, r, tmin, tmax);
-        if (A.M.iso_on && !A.walk_iso) tmax = A.iso_tend[slot];
-        int sp = 0;
-        for (int k = m - 1; k >= 1; k--, sp++) {  // entries 1.. on the stack, entry 1 on top
-            st_code[sp] = res[1 + 3 * k];
-            st_tn[sp] = __int_as_float(res[2 + 3 * k]);
-            st_tf[sp] = __int_as_float(res[3 + 3 * k]);
-        }
-        for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
-        const int lraw = A.leaf_count[slot];
-        W = WalkLane{res[1], (double)__int_as_float(res[2]), (double)__int_as_float(res[3]), sp,
-                     lraw & kLeafCountMask, lraw & kLeafHeavy, INFINITY, 0.f};
-        return true;
-    }
-    if (!spx.live) {
-        A.leaf_count[slot] = 0;
-        return false;
-    }
-    pixel_ray(A, spx.x, spx.y, r);
-    tmin = 0.0;
-    tmax = kTFar;
-    clip_ray(A.M, r, tmin, tmax);
-    const bool clip_ok = tmin < tmax;
-    if (clip_ok && A.M.iso_on && !A.walk_iso) tmax = A.iso_tend[slot];
-    double a = 0.0, b = -1.0;
-    slab_h(S.root_lo, S.root_hi, r, a, b);
-    if (!(clip_ok && S.n_kd > 0 && a <= b && A.wflags[0])) {
-        A.leaf_count[slot] = 0;
-        if (!A.walk_iso) write_empty_pixel(A, slot, spx.out, true);  // no active region
-        return false;
-    }
-    for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
-    W = WalkLane{S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2), a, b, 0, 0, 0, 0.f, 0.f};
-    return true;
-}
-
-template <int PASS>
-__global__ void __launch_bounds__(kWalkThreads) k_walkp(const __grid_constant__ RenderArgs A, int64_t n_slots) {
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    int64_t n_work;
-    if (PASS == 1) {
-        n_work = (int64_t)A.walk_counter[3];
-    } else {
-        const int64_t n_cut = (int64_t)A.walk_counter[2];
-        n_work = n_cut >= A.walk2_min ? n_cut : 0;
-    }
-    unsigned long long* ctr = A.walk_ctr + (PASS - 1);
-    const int cap = PASS == 1 ? A.walk_cap1 : A.leaf_cap;
-    int st_code[kWalkStack];
-    float st_tn[kWalkStack], st_tf[kWalkStack];
-    bool active = false, exhausted = n_work == 0;
-    int64_t ci = 0, slot = 0;
-    SlotPix spx;
-    Ray r;
-    int sg[3] = {0, 0, 0};
-    double tmin = 0.0, tmax = 0.0;
-    WalkLane W{0, 0.0, 0.0, 0, 0, 0, 0.f, 0.f};
-    for (;;) {
-        const unsigned idle = __ballot_sync(FULL, !active);
-        if (idle == FULL && exhausted) break;
-        if (idle && !exhausted) {  // refill the idle lanes
-            const int leader = __ffs(idle) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(ctr, (unsigned long long)__popc(idle));
-            base = __shfl_sync(FULL, base, leader);
-            if ((int64_t)(base + __popc(idle)) >= n_work) exhausted = true;
-            if (!active) {
-                ci = (int64_t)base + __popc(idle & ((1u << lane) - 1u));
-                if (ci < n_work) active = walk_begin<PASS>(A, ci, slot, spx, r, sg, tmin, tmax, W, st_code, st_tn, st_tf);
+    const int64_t n_cand = (int64_t)A.walk_counter[3];
+    // Pass 1 lists at most walk_cap1 leaves per ray: a few very long walks (latency
+    // chains of node loads) would otherwise set the kernel's length; k_walk2
+    // continues the cap-truncated walks when there are many of them.
+    const int cap = A.walk_cap1;
+    if (blockIdx.x * (int64_t)blockDim.x >= n_cand) return;
+    bool is_short = false, is_long = false, is_cut = false;
+    {
+        const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        if (ci >= n_cand) goto route;
+        const int64_t slot = A.hit_list[ci];
+        int count = 0, flags = 0;
+        const SlotPix spx = slot_pixel(A, slot);
+        if (spx.live) {
+            Ray r;
+            pixel_ray(A, spx.x, spx.y, r);
+            double tmin = 0.0, tmax = kTFar;
+            clip_ray(A.M, r, tmin, tmax);
+            const bool clip_ok = tmin < tmax;
+            if (clip_ok && A.M.iso_on && !A.walk_iso) tmax = A.iso_tend[slot];
+            double a = 0.0, b = -1.0;
+            slab_h(S.root_lo, S.root_hi, r, a, b);
+            if (clip_ok && S.n_kd > 0 && a <= b && A.wflags[0]) {
+                int st_code[kWalkStack];
+                float st_tn[kWalkStack], st_tf[kWalkStack];
+                int sg[3];
+                for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
+                float est = 0.f;
+                walk_leaves(A, slot, r, sg, tmin, tmax, S.n_kd4 > 0 ? 0 : -2 - (S.kd[0].a >> 2), a, b, st_code, st_tn,
+                            st_tf, 0, A.leaves + slot * (int64_t)A.leaf_cap, count, flags, cap, est);
+                if (est > A.short_samples) flags |= kLeafHeavy;
             }
-            continue;  // re-ballot: lanes whose ray needed no walk refill again
-        }
-        if (!active) continue;
-        if (walk_step(A, slot, r, sg, tmin, tmax, W, st_code, st_tn, st_tf, A.leaves + slot * (int64_t)A.leaf_cap,
-                      cap))
-            continue;
-        // the walk ended
-        active = false;
-        if (PASS == 1) {
-            if (W.est > A.short_samples) W.flags |= kLeafHeavy;
-            const int v = W.count | W.flags;
-            A.leaf_count[slot] = v;
-            if (W.count == 0 && !W.flags && !A.walk_iso) write_empty_pixel(A, slot, spx.out, true);
-            bool is_short, is_long, is_cut;
-            route_of(A, v, is_short, is_long, is_cut);
-            int32_t* bc = A.blk_counts + 3 * (ci / kWalkThreads);  // k_route's per-128-hit counts
-            if (is_short) atomicAdd(bc, 1);
-            if (is_long) atomicAdd(bc + 1, 1);
-            if (is_cut) atomicAdd(bc + 2, 1);
+            A.leaf_count[slot] = count | flags;
+            if (count == 0 && !flags && !A.walk_iso) write_empty_pixel(A, slot, spx.out, true);  // no active region
         } else {
-            A.leaf_count[slot] = W.count | W.flags;
+            A.leaf_count[slot] = 0;
         }
+        route_of(A, count | flags, is_short, is_long, is_cut);
+    }
+route:
+    // per-block route counts for k_route (block resources are held until the
+    // slowest walk of the block ends anyway, so the barrier costs nothing)
+    const int ns = __syncthreads_count(is_short), nl = __syncthreads_count(is_long),
+              nc = __syncthreads_count(is_cut);
+    if (threadIdx.x == 0) {
+        A.blk_counts[3 * blockIdx.x] = ns;
+        A.blk_counts[3 * blockIdx.x + 1] = nl;
+        A.blk_counts[3 * blockIdx.x + 2] = nc;
     }
     (void)n_slots;
 }
@@ -642,6 +565,39 @@ __global__ void __launch_bounds__(kWalkThreads) k_route(const __grid_constant__ 
 // when there are at least walk2_min of them (decided on the device): many long
 // rays (C2, C5) are cheaper here than in k_warp's frontier; a few (C3) are not.
 
+__global__ void __launch_bounds__(kWalkThreads) k_walk2(const __grid_constant__ RenderArgs A, int64_t n_slots) {
+    const int64_t n_cut = (int64_t)A.walk_counter[2];
+    if (n_cut < A.walk2_min) return;
+    const int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (ci >= n_cut) return;
+    const int64_t slot = A.cut_list[ci];
+    int32_t* res = A.resume + slot * (int64_t)(1 + 3 * kResume);
+    const int m = res[0];
+    if (m <= 0) return;  // remainder not saved: k_warp restarts at the root
+    const SlotPix spx = slot_pixel(A, slot);
+    Ray r;
+    pixel_ray(A, spx.x, spx.y, r);
+    double tmin = 0.0, tmax = kTFar;
+    clip_ray(A.M, r, tmin, tmax);
+    if (A.M.iso_on && !A.walk_iso) tmax = A.iso_tend[slot];
+    int st_code[kWalkStack];
+    float st_tn[kWalkStack], st_tf[kWalkStack];
+    int sp_n = 0;
+    for (int k = m - 1; k >= 1; k--, sp_n++) {  // entries 1.. on the stack, entry 1 on top
+        st_code[sp_n] = res[1 + 3 * k];
+        st_tn[sp_n] = __int_as_float(res[2 + 3 * k]);
+        st_tf[sp_n] = __int_as_float(res[3 + 3 * k]);
+    }
+    int sg[3];
+    for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
+    const int lraw = A.leaf_count[slot];
+    int count = lraw & kLeafCountMask, flags = lraw & kLeafHeavy;
+    float est = INFINITY;
+    walk_leaves(A, slot, r, sg, tmin, tmax, res[1], (double)__int_as_float(res[2]), (double)__int_as_float(res[3]),
+                st_code, st_tn, st_tf, sp_n, A.leaves + slot * (int64_t)A.leaf_cap, count, flags, A.leaf_cap, est);
+    A.leaf_count[slot] = count | flags;
+    (void)n_slots;
+}
 template <bool COUNT>
 __global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const unsigned FULL = 0xffffffffu;
@@ -1578,29 +1534,6 @@ static void hit_select(const RenderArgs& A, int64_t n_slots, cudaStream_t s) {
     XB_CUDA(cudaFreeAsync(tmp, s));
 }
 
-// persistent lane-refill walks (k_walkp): one resident grid; counters and
-// k_route's per-128-hit counts zeroed first (pass 1)
-static void launch_walks(const RenderArgs& A, int64_t n_slots, int pass, cudaStream_t s) {
-    const void* fn = pass == 1 ? (const void*)k_walkp<1> : (const void*)k_walkp<2>;
-    static int grid[2] = {0, 0};
-    if (!grid[pass - 1]) {
-        int dev = 0, sms = 0, per_sm = 0;
-        XB_CUDA(cudaGetDevice(&dev));
-        XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWalkThreads, 0));
-        grid[pass - 1] = std::max(1, sms * std::max(per_sm, 1));
-    }
-    XB_CUDA(cudaMemsetAsync(A.walk_ctr + (pass - 1), 0, sizeof(unsigned long long), s));
-    if (pass == 1) {
-        const int64_t nblk = (n_slots + kWalkThreads - 1) / kWalkThreads;
-        XB_CUDA(cudaMemsetAsync(A.blk_counts, 0, (size_t)std::max<int64_t>(nblk, 1) * 3 * sizeof(int32_t), s));
-    }
-    const int64_t want = (n_slots + kWalkThreads - 1) / kWalkThreads;
-    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid[pass - 1], want));
-    void* args[] = {(void*)&A, (void*)&n_slots};
-    XB_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(kWalkThreads), args, 0, s));
-}
-
 void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaStream_t s) {
     if (n_tiles_local <= 0) return;
     NvtxRange frame_range("xb_render: frame");
@@ -1627,7 +1560,8 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
         XB_CUDA(cudaLaunchKernel((const void*)k_classify, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
                                  iargs, 0, s));
         hit_select(*Ai, n_slots, s);
-        launch_walks(*Ai, n_slots, 1, s);
+        XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads), iargs,
+                                 0, s));
         XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads * kRouteSub)),
                                  dim3(kWalkThreads), iargs, 0, s));
         {
@@ -1670,11 +1604,13 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             hit_select(A, n_slots, s);
             // one thread per candidate (blocks past the device-side count exit at once), then
             // k_route builds the short / long / cut lists
-            launch_walks(A, n_slots, 1, s);
+            XB_CUDA(cudaLaunchKernel((const void*)k_walk, dim3(grid_for(n_slots, kWalkThreads)), dim3(kWalkThreads),
+                                     wargs, 0, s));
             XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads * kRouteSub)),
                                      dim3(kWalkThreads), wargs, 0, s));
             if (A.cut_list && A.walk_cap1 < A.leaf_cap)  // pass 2 over the cap-cut walks
-                launch_walks(A, n_slots, 2, s);
+                XB_CUDA(cudaLaunchKernel((const void*)k_walk2, dim3(grid_for(n_slots, kWalkThreads)),
+                                         dim3(kWalkThreads), wargs, 0, s));
             if (A.short_list && !A.fuse_short) {  // short rays -> k_short (when >= short_min of them)
                 using ShortFn = void (*)(RenderArgs, int64_t);
                 ShortFn sf;
