@@ -122,3 +122,59 @@ def test_websocket_protocol(built):
             ws.send_text(bad.decode())
             err = json.loads(ws.receive_text())
             assert err["type"] == "error" and err["code"] == code
+
+
+def test_concurrent_mixed_renders_and_tf_edits(built):
+    """8 threads render different views, sizes, gradient modes and iso settings of
+    one model concurrently (the reference renders outside its lock,
+    R/service.py:166-176) while another thread keeps rebuilding active sets for
+    new TFs; every frame must equal its sequential render."""
+    from paper_2009_03076_b200.accel import TransferFunction, build_volume_bvh
+    from paper_2009_03076_b200.orbit import orbit_cameras
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame
+
+    model, regions, tree = built
+    lo, hi = model.value_range(0)
+    tf = TransferFunction.grayscale((lo, hi), max_alpha=0.6)
+    scenes = [build_scene(model, regions, tf), build_scene(model, regions, tf, iso_value=0.5 * (lo + hi))]
+    jobs = []
+    for k, (w, h) in enumerate([(64, 48), (96, 64), (40, 40), (128, 72)]):
+        for v, cam in enumerate(orbit_cameras(regions.bounds, 4, w, h)):
+            gm = ("analytic", "central", "none")[(k + v) % 3]
+            jobs.append((scenes[(k + v) % 2], cam, MarchParams(seed=k + v, gradient_mode=gm)))
+    ref = [render_frame(sc, cam, tf, p) for sc, cam, p in jobs]
+    errs, results = [], {}
+    stop = threading.Event()
+
+    def editor():
+        try:
+            a = 0.1
+            while not stop.is_set():
+                build_volume_bvh(regions, TransferFunction.grayscale((lo, hi), max_alpha=a), 0, model=model)
+                a = 0.1 + (a + 0.13) % 0.8
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    def worker(t):
+        try:
+            for rep in range(3):
+                for q in range(t, len(jobs), 8):
+                    sc, cam, p = jobs[q]
+                    results[(q, rep)] = render_frame(sc, cam, tf, p)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ed = threading.Thread(target=editor)
+    ed.start()
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    stop.set()
+    ed.join()
+    assert not errs, errs
+    assert len(results) == 3 * len(jobs)
+    for (q, rep), fr in results.items():
+        assert np.array_equal(fr.rgba, ref[q].rgba), (q, rep)
+        assert (fr.stats.regions, fr.stats.samples) == (ref[q].stats.regions, ref[q].stats.samples)
