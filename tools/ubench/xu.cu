@@ -10,7 +10,7 @@ __global__ void k_f2f(const float* in, double* out) {
     for (int c = 0; c < CH; c++) { v[c] = in[threadIdx.x + c]; acc[c] = 0; }
     for (int i = 0; i < ITERS; i++)
 #pragma unroll
-        for (int c = 0; c < CH; c++) { acc[c] ^= __double_as_longlong((double)v[c]); v[c] = __int_as_float(__float_as_int(v[c]) ^ (i & 1)); }
+        for (int c = 0; c < CH; c++) { acc[c] ^= __double_as_longlong((double)v[c]); v[c] = __int_as_float(__float_as_int(v[c]) + 1); }
     double s = 0; for (int c = 0; c < CH; c++) s += (double)acc[c];
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
@@ -19,7 +19,7 @@ __global__ void k_i2f(const int* in, double* out) {
     for (int c = 0; c < CH; c++) { v[c] = in[threadIdx.x + c]; acc[c] = 0; }
     for (int i = 0; i < ITERS; i++)
 #pragma unroll
-        for (int c = 0; c < CH; c++) { acc[c] ^= __double_as_longlong((double)v[c]); v[c] ^= (i & 1); }
+        for (int c = 0; c < CH; c++) { acc[c] ^= __double_as_longlong((double)v[c]); v[c] += 1; }
     double s = 0; for (int c = 0; c < CH; c++) s += (double)acc[c];
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
