@@ -100,6 +100,7 @@ struct SceneView {
     // frame-gather brick records in region-list order (rb[i] = brick rids[i]):
     // a region's bricks are read without the id hop
     const struct RbRec* __restrict__ rb;
+    const int4* __restrict__ rb16;  // XB_REC16 builds: the 16-B records (decode_rb16)
     const KdNode* __restrict__ kd;
     const Kd4Node* __restrict__ kd4;
     int32_t root_lo[3], root_hi[3];
@@ -594,6 +595,22 @@ __device__ __forceinline__ RbRec load_rb(const RbRec* __restrict__ p) {
     return r;
 }
 
+// 16-byte variant of the record (XB_REC16): the lower corner in cells of the
+// brick's own level as three signed 21-bit fields (x | y << 21 | z << 42),
+// the scalar offset and the meta word — one 16-B load; the corner is decoded
+// as (double)cells * w (exact).  Built only when every corner fits.
+__device__ __forceinline__ RbRec decode_rb16(const int4 q) {
+    const unsigned long long xyz = ((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x;
+    const double w = pow2(q.w & 31);
+    RbRec r;
+    r.lx = (double)(int)((long long)(xyz << 43) >> 43) * w;
+    r.ly = (double)(int)((long long)(xyz << 22) >> 43) * w;
+    r.lz = (double)(int)((long long)(xyz << 1) >> 43) * w;
+    r.off = (uint32_t)q.z;
+    r.meta = (uint32_t)q.w;
+    return r;
+}
+
 // Running state of the frame gather of one sample (value sums in the
 // reference's exact FP64 sequence; FP32 shading-gradient partials).  Pairing
 // the FP32 partials over dz on sm_100's f32x2 instructions cut brick_step from
@@ -732,6 +749,19 @@ __device__ __forceinline__ void brick_step(const SceneView& S, const RbRec& B, d
         A.dd1 = fmaf(Hx * Sy, Hz, A.dd1);
         A.dd2 = fmaf(Hx * Hy, Sz, A.dd2);
     }
+}
+
+// the frame gather over a warp's staged 16-B records (shared memory)
+template <bool GRAD>
+__device__ __forceinline__ void gather_staged(const SceneView& S, const int4* __restrict__ recs, int nids, double px,
+                                              double py, double pz, FastAccum& F) {
+    ShadeAcc A;
+    A.clear();
+    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, decode_rb16(recs[t]), px, py, pz, A);
+    F.num = A.num;
+    F.den = A.den;
+    F.n_nz = A.n_nz;
+    if (GRAD) A.gradient(F.g);
 }
 
 // the frame gather over region-list entries [off, off + nids) (S.rb)

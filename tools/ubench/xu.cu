@@ -63,6 +63,34 @@ __global__ void k_ffma(const double* in, double* out) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_frnd(const double* in, double* out) {
+    double v[CH]; long long acc[CH];
+    for (int c = 0; c < CH; c++) { v[c] = in[threadIdx.x + c] + 0.5; acc[c] = 0; }
+    for (int i = 0; i < ITERS; i++)
+#pragma unroll
+        for (int c = 0; c < CH; c++) { acc[c] ^= __double_as_longlong(floor(v[c])); v[c] = __longlong_as_double(__double_as_longlong(v[c]) + 1); }
+    double s = 0; for (int c = 0; c < CH; c++) s += (double)acc[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_d2f(const double* in, double* out) {
+    double v[CH]; int acc[CH];
+    for (int c = 0; c < CH; c++) { v[c] = in[threadIdx.x + c] + 0.5; acc[c] = 0; }
+    for (int i = 0; i < ITERS; i++)
+#pragma unroll
+        for (int c = 0; c < CH; c++) { acc[c] ^= __float_as_int((float)v[c]); v[c] = __longlong_as_double(__double_as_longlong(v[c]) + (1ll << 30)); }
+    double s = 0; for (int c = 0; c < CH; c++) s += (double)acc[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_lop(const double* in, double* out) {
+    int v[CH];
+    for (int c = 0; c < CH; c++) v[c] = (int)in[threadIdx.x + c];
+    const int m = (int)in[0] + 0x1234;
+    for (int i = 0; i < ITERS; i++)
+#pragma unroll
+        for (int c = 0; c < CH; c++) v[c] = (v[c] ^ m) + c;
+    double s = 0; for (int c = 0; c < CH; c++) s += v[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
 template <class F, class T>
 void run(const char* name, F kern, T* in, double* out, int sms) {
     cudaEvent_t a, b;
@@ -92,5 +120,8 @@ int main() {
     run("DADD", k_dadd, din, out, sms);
     run("DFMA", k_dfma, din, out, sms);
     run("FFMA", k_ffma, din, out, sms);
+    run("FRND.F64", k_frnd, din, out, sms);
+    run("F2F.F32.F64", k_d2f, din, out, sms);
+    run("IADD+LOP", k_lop, din, out, sms);
     return 0;
 }
