@@ -23,6 +23,9 @@ namespace xb {
 
 constexpr double kEpsWeight = 1e-12;     // EPS_WEIGHT, R/sampling.py:37
 
+#ifndef XB_MAGIC_FLOOR
+#define XB_MAGIC_FLOOR 0
+#endif
 #ifndef XB_GATHER_VARIANT
 #define XB_GATHER_VARIANT 0
 #endif
@@ -652,8 +655,19 @@ struct Axis2 {
 __device__ __forceinline__ Axis2 window_axis(double p, double l, int n, double w, double iw, float fw) {
     Axis2 A;
     const double t = __fma_rn(p - l, iw, -0.5);
+#if XB_MAGIC_FLOOR
+    // floor(t) without the conversion unit (I2F.F64 / FRND run at 1/4 of the
+    // DADD rate on B200, tools/ubench/xu.cu): t + 1.5*2^52 holds round(t) in
+    // its low word (|t| < 2^51), subtracting it back gives round(t) exactly
+    const double big = t + 6755399441055744.0;
+    double fx = big - 6755399441055744.0;
+    A.x0 = __double2loint(big);
+    if (fx > t) { fx -= 1.0; A.x0 -= 1; }
+    const double c0 = __fma_rn(fx + 0.5, w, l);  // exact: l + (x0 + 1/2) w
+#else
     A.x0 = __double2int_rd(t);
     const double c0 = __fma_rn((double)A.x0 + 0.5, w, l);  // exact: l + (x0 + 1/2) w
+#endif
     const double e0 = c0 - p, e1 = (c0 + w) - p;
     const double h0 = __fma_rn(-fabs(e0), iw, 1.0), h1 = __fma_rn(-fabs(e1), iw, 1.0);
 #if XB_INT_TESTS
