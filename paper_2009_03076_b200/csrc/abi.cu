@@ -36,7 +36,6 @@ struct xb_regions {
     // brick records in region-list order for the frame gather (built on first render)
     mutable std::mutex rb_mu;
     mutable xb::DevBuf<xb::RbRec> rb;
-    mutable xb::DevBuf<int4> rb16;  // 16-B records (XB_REC16 / XB_STAGE builds)
     mutable bool rb_ok = false;
 };
 struct xb_active {
@@ -105,8 +104,7 @@ constexpr int64_t kBandSlots = 1ll << 22;
 
 // frame-gather brick records in region-list order (march.cuh:RbRec)
 __global__ void k_region_bricks(const int32_t* __restrict__ ids, int64_t n, const int4* __restrict__ ba,
-                                const uint32_t* __restrict__ bm, xb::RbRec* __restrict__ rb, int4* __restrict__ rb16,
-                                int* __restrict__ overflow) {
+                                const uint32_t* __restrict__ bm, xb::RbRec* __restrict__ rb) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int b = ids[i];
@@ -118,16 +116,6 @@ __global__ void k_region_bricks(const int32_t* __restrict__ ids, int64_t n, cons
     r.off = (uint32_t)a.w;
     r.meta = bm[b];
     rb[i] = r;
-    if (rb16) {  // lower corner in cells of the brick's level, 3 x signed 21 bits
-        const int lev = r.meta & 31;
-        const int cx = a.x >> lev, cy = a.y >> lev, cz = a.z >> lev;  // corners are multiples of 2^lev
-        const int lim = 1 << 20;
-        if (cx < -lim || cx >= lim || cy < -lim || cy >= lim || cz < -lim || cz >= lim) *overflow = 1;
-        const unsigned long long xyz = ((unsigned long long)(cx & 0x1fffff)) |
-                                       ((unsigned long long)(cy & 0x1fffff) << 21) |
-                                       ((unsigned long long)(cz & 0x1fffff) << 42);
-        rb16[i] = make_int4((int)(unsigned)(xyz & 0xffffffffu), (int)(unsigned)(xyz >> 32), a.w, (int)r.meta);
-    }
 }
 
 void ensure_region_bricks(const xb_model* m, const xb_regions* r) {
@@ -135,17 +123,12 @@ void ensure_region_bricks(const xb_model* m, const xb_regions* r) {
     if (r->rb_ok) return;
     const int64_t n = std::max<int64_t>(r->r.n_ids, 1);
     r->rb.alloc(n);
-    if (XB_STAGE) r->rb16.alloc(n);
     if (r->r.n_ids > 0) {
         OwnedStream st;
-        xb::DevBuf<int> ovf(1);
-        XB_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), st.s));
         k_region_bricks<<<(unsigned)((r->r.n_ids + 255) / 256), 256, 0, st.s>>>(
-            r->r.ids.p, r->r.n_ids, m->m.brick_a.p, m->m.brick_m.p, r->rb.p, XB_STAGE ? r->rb16.p : nullptr, ovf.p);
+            r->r.ids.p, r->r.n_ids, m->m.brick_a.p, m->m.brick_m.p, r->rb.p);
         XB_CUDA(cudaGetLastError());
         XB_CUDA(cudaStreamSynchronize(st.s));
-        XB_CHECK(xb::read_scalar(ovf.p, st.s) == 0, XB_ERR_RANGE,
-                 "brick corners exceed the 16-byte record's 21-bit range (XB_STAGE build)");
     }
     r->rb_ok = true;
 }
@@ -183,7 +166,6 @@ xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     S.rids = r->r.ids.p;
     ensure_region_bricks(m, r);
     S.rb = r->rb.p;
-    S.rb16 = r->rb16.p;
     S.kd = r->r.kd.p;
     S.kd4 = r->r.kd4.p;
     for (int a = 0; a < 3; a++) {

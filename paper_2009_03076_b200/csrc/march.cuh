@@ -23,15 +23,6 @@ namespace xb {
 
 constexpr double kEpsWeight = 1e-12;     // EPS_WEIGHT, R/sampling.py:37
 
-#ifndef XB_MAGIC_FLOOR
-#define XB_MAGIC_FLOOR 0
-#endif
-#ifndef XB_GATHER_VARIANT
-#define XB_GATHER_VARIANT 0
-#endif
-#ifndef XB_INT_TESTS
-#define XB_INT_TESTS 1
-#endif
 constexpr double kTFar = 1.0e30;
 // zero pad around the frame gather's value copy: a brick's unclamped 2x2x2
 // window reaches at most nx*(ny+1) + 1 <= 32*33 + 1 values before or after it
@@ -103,7 +94,6 @@ struct SceneView {
     // frame-gather brick records in region-list order (rb[i] = brick rids[i]):
     // a region's bricks are read without the id hop
     const struct RbRec* __restrict__ rb;
-    const int4* __restrict__ rb16;  // XB_REC16 builds: the 16-B records (decode_rb16)
     const KdNode* __restrict__ kd;
     const Kd4Node* __restrict__ kd4;
     int32_t root_lo[3], root_hi[3];
@@ -598,22 +588,6 @@ __device__ __forceinline__ RbRec load_rb(const RbRec* __restrict__ p) {
     return r;
 }
 
-// 16-byte variant of the record (XB_REC16): the lower corner in cells of the
-// brick's own level as three signed 21-bit fields (x | y << 21 | z << 42),
-// the scalar offset and the meta word — one 16-B load; the corner is decoded
-// as (double)cells * w (exact).  Built only when every corner fits.
-__device__ __forceinline__ RbRec decode_rb16(const int4 q) {
-    const unsigned long long xyz = ((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x;
-    const double w = pow2(q.w & 31);
-    RbRec r;
-    r.lx = (double)(int)((long long)(xyz << 43) >> 43) * w;
-    r.ly = (double)(int)((long long)(xyz << 22) >> 43) * w;
-    r.lz = (double)(int)((long long)(xyz << 1) >> 43) * w;
-    r.off = (uint32_t)q.z;
-    r.meta = (uint32_t)q.w;
-    return r;
-}
-
 // Running state of the frame gather of one sample (value sums in the
 // reference's exact FP64 sequence; FP32 shading-gradient partials).  Pairing
 // the FP32 partials over dz on sm_100's f32x2 instructions cut brick_step from
@@ -655,22 +629,10 @@ struct Axis2 {
 __device__ __forceinline__ Axis2 window_axis(double p, double l, int n, double w, double iw, float fw) {
     Axis2 A;
     const double t = __fma_rn(p - l, iw, -0.5);
-#if XB_MAGIC_FLOOR
-    // floor(t) without the conversion unit (I2F.F64 / FRND run at 1/4 of the
-    // DADD rate on B200, tools/ubench/xu.cu): t + 1.5*2^52 holds round(t) in
-    // its low word (|t| < 2^51), subtracting it back gives round(t) exactly
-    const double big = t + 6755399441055744.0;
-    double fx = big - 6755399441055744.0;
-    A.x0 = __double2loint(big);
-    if (fx > t) { fx -= 1.0; A.x0 -= 1; }
-    const double c0 = __fma_rn(fx + 0.5, w, l);  // exact: l + (x0 + 1/2) w
-#else
     A.x0 = __double2int_rd(t);
     const double c0 = __fma_rn((double)A.x0 + 0.5, w, l);  // exact: l + (x0 + 1/2) w
-#endif
     const double e0 = c0 - p, e1 = (c0 + w) - p;
     const double h0 = __fma_rn(-fabs(e0), iw, 1.0), h1 = __fma_rn(-fabs(e1), iw, 1.0);
-#if XB_INT_TESTS
     // sign tests on the high words (integer pipe; the FP64 pipe is the gather's
     // bottleneck).  For a double x that is 0, normal, or negative, x > 0.0 <=> its
     // high word is > 0 as a signed int; subnormal h or e cannot occur here (h is
@@ -679,12 +641,6 @@ __device__ __forceinline__ Axis2 window_axis(double p, double l, int n, double w
     A.v1 = (unsigned)(A.x0 + 1) < (unsigned)n && __double2hiint(h1) > 0;
     A.s0 = A.v0 ? (__double2hiint(e0) > 0 ? fw : -fw) : 0.f;
     A.s1 = A.v1 ? (__double2hiint(e1) > 0 ? fw : -fw) : 0.f;
-#else
-    A.v0 = (unsigned)A.x0 < (unsigned)n && h0 > 0.0;
-    A.v1 = (unsigned)(A.x0 + 1) < (unsigned)n && h1 > 0.0;
-    A.s0 = A.v0 ? (e0 > 0.0 ? fw : -fw) : 0.f;
-    A.s1 = A.v1 ? (e1 > 0.0 ? fw : -fw) : 0.f;
-#endif
     A.h0 = A.v0 ? h0 : 0.0;
     A.h1 = A.v1 ? h1 : 0.0;
     return A;
@@ -765,19 +721,6 @@ __device__ __forceinline__ void brick_step(const SceneView& S, const RbRec& B, d
     }
 }
 
-// the frame gather over a warp's staged 16-B records (shared memory)
-template <bool GRAD>
-__device__ __forceinline__ void gather_staged(const SceneView& S, const int4* __restrict__ recs, int nids, double px,
-                                              double py, double pz, FastAccum& F) {
-    ShadeAcc A;
-    A.clear();
-    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, decode_rb16(recs[t]), px, py, pz, A);
-    F.num = A.num;
-    F.den = A.den;
-    F.n_nz = A.n_nz;
-    if (GRAD) A.gradient(F.g);
-}
-
 // the frame gather over region-list entries [off, off + nids) (S.rb)
 template <bool GRAD>
 __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, int nids, double px, double py,
@@ -785,20 +728,7 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, in
     ShadeAcc A;
     A.clear();
     const RbRec* __restrict__ rb = S.rb + off;
-#if XB_GATHER_VARIANT == 1
-#pragma unroll 2
     for (int t = 0; t < nids; t++) brick_step<GRAD>(S, load_rb(rb + t), px, py, pz, A);
-#elif XB_GATHER_VARIANT == 2
-    // software pipeline: the next brick record is in flight while this brick runs
-    RbRec cur = load_rb(rb);
-    for (int t = 0; t < nids; t++) {
-        const RbRec nxt = load_rb(rb + min(t + 1, nids - 1));
-        brick_step<GRAD>(S, cur, px, py, pz, A);
-        cur = nxt;
-    }
-#else
-    for (int t = 0; t < nids; t++) brick_step<GRAD>(S, load_rb(rb + t), px, py, pz, A);
-#endif
     F.num = A.num;
     F.den = A.den;
     F.n_nz = A.n_nz;

@@ -139,7 +139,6 @@ constexpr int kWarpThreads = 128;
 #endif
 constexpr int kWarpMinBlocks = XB_WARP_MINB;
 constexpr int kWarpsPerBlock = kWarpThreads / 32;
-constexpr int kStageCap = 64;  // XB_STAGE builds: staged 16-B records per warp (static smem < 48 KB)
 constexpr int kWarpStack = 256;  // spilled frontier entries per warp
 constexpr int kRaysPerGrab = 8;  // rays taken per work-counter atomic
 // A (sample, brick)-flattened chunk gather (each lane one brick per round,
@@ -871,9 +870,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     __shared__ SegQ s_q[kWarpsPerBlock][32];
     __shared__ RayAxes s_ray[kWarpsPerBlock];
     __shared__ RaySetup s_setup[kWarpsPerBlock][32];
-#if XB_STAGE
-    __shared__ int4 s_rb[kWarpsPerBlock][kStageCap];
-#endif
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
     __syncthreads();
     const unsigned FULL = 0xffffffffu;
@@ -1054,41 +1050,9 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             }
                         }
                         FastAccum F;
-#if XB_STAGE
-                        {
-                            // stage the brick records of the chunk's segments (window positions
-                            // sg(lane 0) .. sg(lane m-1)), one lane per segment, then gather from
-                            // shared memory; chunks with more than kStageCap records read global
-                            const int sg0 = __shfl_sync(FULL, sg, 0), sg1 = __shfl_sync(FULL, sg, m - 1);
-                            int segL = 0, segIds = 0;
-                            if (lane <= sg1 - sg0) {
-                                const SegQ& e = ring[(qh + sg0 + lane) & 31];
-                                segL = e.meta & 0xffffff;
-                                segIds = e.ids;
-                            }
-                            int pre = segL;
-#pragma unroll
-                            for (int o = 1; o < 32; o <<= 1) {
-                                const int v = __shfl_up_sync(FULL, pre, o);
-                                if (lane >= o) pre += v;
-                            }
-                            const int total = __shfl_sync(FULL, pre, 31);
-                            pre -= segL;
-                            const int my_off = __shfl_sync(FULL, pre, max(sg - sg0, 0) & 31);
-                            __syncwarp();  // the previous chunk's reads of s_rb are done
-                            if (total <= kStageCap) {
-                                for (int t = 0; t < segL; t++) s_rb[wid][pre + t] = __ldg(S.rb16 + segIds + t);
-                                __syncwarp();
-                                if (act) gather_staged<GRAD == 1>(S, &s_rb[wid][my_off], nids, px, py, pz, F);
-                            } else if (act) {
-                                gather_shade<GRAD == 1>(S, (int64_t)sq.ids, nids, px, py, pz, F);
-                            }
-                        }
-#else
                         if (act) {
                             gather_shade<GRAD == 1>(S, (int64_t)sq.ids, nids, px, py, pz, F);
                         }
-#endif
                         if (act) {
                             if (COUNT) my_bytes = 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
                             if (F.den > kEpsWeight) {

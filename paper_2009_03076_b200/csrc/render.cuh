@@ -12,11 +12,6 @@ constexpr int kWalkThreads = 128;  // k_classify / k_walk / k_route / k_short bl
 constexpr float kShortSamples = 24.f;  // short ray: complete list of <= kShortLeaves leaves, <= kShortSamples
 constexpr int kShortLeaves = 8;        // estimated samples (RenderArgs.short_samples / short_leaves)
 constexpr int kResume = 48;            // resume entries saved per truncated walk
-// XB_STAGE builds: a chunk's brick records (16-B form, march.cuh:decode_rb16) are
-// staged per warp in shared memory before the gather (north_star's per-ABR staging)
-#ifndef XB_STAGE
-#define XB_STAGE 0
-#endif
 // k_warp work statistics, compiled in only with `make DEBUG_CHUNKS=1` (the counters cost k_warp registers)
 #ifndef XB_DEBUG_CHUNKS
 #define XB_DEBUG_CHUNKS 0

@@ -1,6 +1,7 @@
 """Oracle digests of the builders at the benchmarked scales (test fixture).
 
   python tools/make_scale_digests.py c2 c3
+  XB_DIGESTS_OUT=gpurun_out/scale_digests_c5.json python tools/make_scale_digests.py c5   # on the GPU box (RAM)
 
 For each bench config: the cells from the numpy generator (bit-exact
 restatement of the reference's generate_synthetic, R/io.py:247-295, pinned by
@@ -22,7 +23,7 @@ import bench  # noqa: E402
 import oracle  # noqa: E402
 from tests_util import sha  # noqa: E402
 
-OUT = ROOT / "tests" / "golden" / "scale_digests.json"
+OUT = Path(os.environ.get("XB_DIGESTS_OUT", ROOT / "tests" / "golden" / "scale_digests.json"))
 MODEL_KEYS = ("brick_lower", "brick_level", "brick_dims", "brick_offset", "scalars")
 REGION_KEYS = ("lo", "hi", "brick_off", "brick_ids", "value_range", "finest_width")
 
@@ -32,7 +33,7 @@ def main():
     for name in sys.argv[1:]:
         cfg = bench.CONFIGS[name]
         t0 = time.time()
-        cells = bench.make_cells(dict(cfg, gpu_gen=False), host=True)
+        cells = bench.make_cells(dict(cfg, gpu_gen=False), host=True)  # the numpy generator
         t1 = time.time()
         m = oracle.build_bricks(cells.i, cells.j, cells.k, cells.level, cells.values)
         t2 = time.time()
