@@ -77,8 +77,7 @@ CONFIGS = {
                workload="configs[3]: Landing-Gear-shaped AMR (266M cells), implicit iso-surface 0.5 + DVR, "
                         "1920x1080, with a TF-edit active-set/majorant refresh"),
     # C5: Exajet-shaped, 4 levels, hole/refine chain along x (SURVEY.md §8(d) template), 647M cells
-    # from the GPU generator (csrc/synth.cu; bit-exact to the reference generator's digests)
-    "c5": dict(spec="jet", gpu_gen=True, res=(1920, 1080), max_alpha=0.5, gradient="analytic",
+    "c5": dict(spec="jet", res=(1920, 1080), max_alpha=0.5, gradient="analytic",
                workload="configs[4]: synthetic Exajet-shaped AMR (4 levels, 647M cells), 1920x1080 DVR + analytic shading"),
 }
 JET = dict(thr=0.003, rh=80.0, rr=300.0, step=80.0, sigma=400.0)  # 647,115,612 cells (tools/calib.py)
@@ -160,8 +159,8 @@ def host_info():
 def make_cells(cfg, host=False):
     """Synthetic cells of a config: the numpy generator (C1-C4: a bit-exact
     restatement of the reference's generate_synthetic, R/io.py:247-295, run on
-    all host cores) or the GPU generator (C5's 647M cells; left on the device
-    unless `host`)."""
+    all host cores; every bench config) or the GPU generator (`gpu_gen`, cells
+    left on the device unless `host`)."""
     from paper_2009_03076_b200 import io as xio
 
     spec = spec_for(cfg)
@@ -667,6 +666,8 @@ def bench_ours(args):
         line = {"metric": METRIC, "value": res["value"], "unit": "frames/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "dtype_note": "FP64 sample positions, hat weights, value sums, TF and compositing (the reference's "
+                              "arithmetic); the analytic gradient that only feeds the headlight factor is FP32",
                 "config": workload_config(cfg, args.views, S.n_cells, S.model.n_bricks, len(S.regions))}
         line.update({k: res[k] for k in ("msamples_per_s", "kernel_ms", "frame", "roofline", "views")})
         line["method"] = {"l2": "flushed between frames (256 MB write)", "parallelism": f"screen tiles 16x8 x{world}",
@@ -754,6 +755,10 @@ def bench_ours(args):
             if rank == 0:
                 line_extra[name] = dict(rx, config=workload_config(cfg_x, args.views, Sx.n_cells, Sx.model.n_bricks,
                                                                    len(Sx.regions)), build_ms=Sx.build_ms)
+                if Sx.build_ms and "bricks" in Sx.build_ms:  # a model of its own: its builder parity
+                    pb = Sx.builder_parity()
+                    line_extra[name]["parity"] = {"builders": pb}
+                    ok = ok and (pb or {"equal": True})["equal"]
             del Sx
             torch.cuda.empty_cache()
         if rank == 0:
