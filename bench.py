@@ -573,12 +573,23 @@ def frame_parity(S, bands):
 
 
 def e2e_orbit(S, steps):
-    """render_frame() through the public API: host RGBA8 out, stats read back, cycling the orbit."""
+    """The public API with host output, cycling the orbit: `render_frames` (the
+    host copy of frame k overlaps the march of frame k+1; wall time over the K
+    frames) and `render_frame` (one synchronous call per frame)."""
     import torch
 
-    from paper_2009_03076_b200.render import render_frame
+    from paper_2009_03076_b200.render import render_frame, render_frames
 
     V = len(S.cams)
+    cams = [S.cams[k % V] for k in range(steps)]
+    for fr in render_frames(S.scene, cams[:3], S.tf, S.params):
+        pass
+    torch.cuda.synchronize()
+    ta = time.perf_counter()
+    n = 0
+    for fr in render_frames(S.scene, cams, S.tf, S.params):
+        n += fr.stats.samples > 0
+    pipelined_ms = (time.perf_counter() - ta) * 1e3 / steps
     for k in range(3):
         render_frame(S.scene, S.cams[k % V], S.tf, S.params)
     torch.cuda.synchronize()
@@ -587,7 +598,7 @@ def e2e_orbit(S, steps):
         ta = time.perf_counter()
         render_frame(S.scene, S.cams[k % V], S.tf, S.params)
         ts.append((time.perf_counter() - ta) * 1e3)
-    return ts
+    return pipelined_ms, ts
 
 
 def ablations(S, dev):
@@ -689,14 +700,18 @@ def bench_ours(args):
             line["nccl"] = nccl
     if full:
         if world == 1:
-            e2e = e2e_orbit(S, args.steps)
+            pipe_ms, e2e = e2e_orbit(S, args.steps)
             import ctypes
 
-            line["e2e"] = {"value": 1000.0 * len(e2e) / sum(e2e), "unit": "frames/s",
+            line["e2e"] = {"value": 1000.0 / pipe_ms, "unit": "frames/s",
                            "h2d_bytes_per_step": ctypes.sizeof(N.XbMarch) + ctypes.sizeof(N.XbCamera),
                            "d2h_bytes_per_step": cfg["res"][0] * cfg["res"][1] * 4 + 24,
-                           "ms_per_step": float(np.mean(e2e)), "ms_steps": [round(x, 3) for x in e2e],
-                           "api": "render_frame() -> numpy Frame (RGBA8 + FrameStats), orbit views"}
+                           "ms_per_step": pipe_ms,
+                           "api": "render_frames(scene, orbit cameras, tf, params) -> numpy Frames (RGBA8 + "
+                                  "FrameStats; each frame's D2H overlaps the next frame's march)",
+                           "sync": {"value": 1000.0 * len(e2e) / sum(e2e), "ms_per_step": float(np.mean(e2e)),
+                                    "ms_steps": [round(x, 3) for x in e2e],
+                                    "api": "render_frame() per frame (synchronous)"}}
         else:
             e2e_ms = e2e_tiled(S, rend, args.steps, world, rank, dev)
             if rank == 0:

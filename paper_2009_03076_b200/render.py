@@ -25,7 +25,8 @@ from .regions import RegionSet
 
 __all__ = [
     "Camera", "MarchParams", "FrameStats", "Frame", "Scene", "build_scene", "make_intervals", "opacity_correct",
-    "shade", "pixel_rho", "integrate_ray", "iso_intersect", "render_frame", "render_frame_float", "GRADIENT_MODES",
+    "shade", "pixel_rho", "integrate_ray", "iso_intersect", "render_frame", "render_frames", "render_frame_float",
+    "GRADIENT_MODES",
     "ISO_COLOR",
 ]
 
@@ -335,6 +336,60 @@ def render_frame(scene: Scene, camera: Camera, tf: TransferFunction, params: Mar
     stats = render_native(scene, camera, tf, params, out, use_celllocation=use_celllocation)
     ms = (time.perf_counter() - t0) * 1000.0
     return Frame(camera.width, camera.height, out, FrameStats(ms, int(stats[0]), int(stats[1])))
+
+
+def render_frames(scene: Scene, cameras, tf: TransferFunction, params: MarchParams):
+    """Render a sequence of frames (an orbit, an animation) with the host copy
+    of frame k overlapping the march of frame k+1; yields one `Frame` per camera,
+    in order, each with its host RGBA8 (page-locked) and `FrameStats` (`ms` =
+    the frame's GPU time from CUDA events; the frames are pixel-identical to
+    `render_frame`).  Two device images alternate: the march runs on one
+    stream, the device-to-host copies on another, joined by events."""
+    import torch
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    s_march, s_copy = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    slots = []  # (device image, device stats, copy-done event)
+    pending = []  # frames in flight: (camera, host image, host stats, march start/end events, copy event)
+    k = 0
+    for cam in cameras:
+        if cam.width < 1 or cam.height < 1:
+            raise ValueError("image must be at least 1x1 pixel")
+        if len(slots) < 2:
+            slots.append([torch.empty((cam.height, cam.width, 4), dtype=torch.uint8, device=dev),
+                          torch.zeros(3, dtype=torch.int64, device=dev), None])
+        img, st, done = slots[k % 2]
+        if img.shape != (cam.height, cam.width, 4):
+            img = slots[k % 2][0] = torch.empty((cam.height, cam.width, 4), dtype=torch.uint8, device=dev)
+        if done is not None:
+            s_march.wait_event(done)  # this slot's previous copy has left the device
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s_march)
+        render_native(scene, cam, tf, params, img.data_ptr(), stream=s_march.cuda_stream, sync=False,
+                      dev_stats=st.data_ptr())
+        b.record(s_march)
+        host = torch.empty((cam.height, cam.width, 4), dtype=torch.uint8, pin_memory=True)
+        hst = torch.empty(3, dtype=torch.int64, pin_memory=True)
+        s_copy.wait_event(b)
+        with torch.cuda.stream(s_copy):
+            host.copy_(img, non_blocking=True)
+            hst.copy_(st, non_blocking=True)
+        c = torch.cuda.Event()
+        c.record(s_copy)
+        slots[k % 2][2] = c
+        pending.append((cam, host, hst, a, b, c))
+        k += 1
+        if len(pending) == 2:  # frame k-1 is ready once its copy is
+            yield _finish_pending(pending.pop(0))
+    while pending:
+        yield _finish_pending(pending.pop(0))
+
+
+def _finish_pending(p):
+    cam, host, hst, a, b, c = p
+    c.synchronize()
+    st = hst.numpy()
+    return Frame(cam.width, cam.height, host.numpy(), FrameStats(a.elapsed_time(b), int(st[0]), int(st[1])))
 
 
 def render_frame_float(scene: Scene, camera: Camera, tf: TransferFunction, params: MarchParams, count_bytes=False,

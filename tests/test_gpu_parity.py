@@ -573,3 +573,28 @@ def test_large_frames_render_in_bands(xb):
     assert (fr.stats.regions, fr.stats.samples) == (int(st[0]), int(st[1])) == (int(cnt[..., 0].sum()),
                                                                                int(cnt[..., 1].sum()))
     assert fr.stats.samples > 0
+
+
+def test_render_frames_pipeline_equals_render_frame(xb):
+    """render_frames (march of frame k+1 overlapping the copy of frame k) returns the
+    same frames, in order, as one render_frame call per camera."""
+    from paper_2009_03076_b200.accel import TransferFunction
+    from paper_2009_03076_b200.orbit import orbit_cameras, run_bench
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame, render_frames
+
+    model, _, regions = _build("smoke")
+    lo, hi = model.value_range(0)
+    tf = TransferFunction.grayscale((lo, hi), max_alpha=0.5)
+    scene = build_scene(model, regions, tf)
+    cams = orbit_cameras(regions.bounds, 5, 120, 80) + orbit_cameras(regions.bounds, 3, 64, 48)
+    params = MarchParams(seed=4, gradient_mode="analytic")
+    got = list(render_frames(scene, cams, tf, params))
+    assert len(got) == len(cams)
+    for cam, fr in zip(cams, got):
+        ref = render_frame(scene, cam, tf, params)
+        assert fr.rgba.shape == ref.rgba.shape and np.array_equal(fr.rgba, ref.rgba)
+        assert (fr.stats.regions, fr.stats.samples) == (ref.stats.regions, ref.stats.samples)
+        assert fr.stats.ms > 0
+    rows, _ = run_bench(scene, tf, params, 4, 96, 64, pipelined=True)
+    rows2, _ = run_bench(scene, tf, params, 4, 96, 64)
+    assert [(r.regions, r.samples) for r in rows] == [(r.regions, r.samples) for r in rows2]
