@@ -8,7 +8,10 @@ constexpr int kTileW = 16, kTileH = 8;  // screen tile; a warp owns an 8x4 quart
 
 // Passed by value as a __grid_constant__ kernel parameter (~8.6 KB < 32 KB):
 // the call needs no device allocation, so concurrent renders are reentrant.
-constexpr int kWalkThreads = 128;  // k_classify / k_walk / k_route / k_short block size
+#ifndef XB_WALK_THREADS
+#define XB_WALK_THREADS 128
+#endif
+constexpr int kWalkThreads = XB_WALK_THREADS;  // k_classify / k_walk / k_route / k_short block size
 constexpr float kShortSamples = 24.f;  // short ray: complete list of <= kShortLeaves leaves, <= kShortSamples
 constexpr int kShortLeaves = 8;        // estimated samples (RenderArgs.short_samples / short_leaves)
 constexpr int kResume = 48;            // resume entries saved per truncated walk
