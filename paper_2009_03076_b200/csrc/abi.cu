@@ -776,7 +776,6 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->work_counter = scratch + 3;
         A->dbg = xb::kDebugChunks ? scratch + 9 : nullptr;  // [9, 16): make DEBUG_CHUNKS=1 builds only
         A->short_counter = scratch + 16;
-        A->walk_ctr = scratch + 17;
         A->fuse_short = T.fuse_short != 0;
         A->grab_div = 4;
         A->grab_fixed = 0;

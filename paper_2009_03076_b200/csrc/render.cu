@@ -604,240 +604,6 @@ __global__ void __launch_bounds__(kWalkThreads) k_walk2(const __grid_constant__ 
     A.leaf_count[slot] = count | flags;
     (void)n_slots;
 }
-// Pass 2, warp-cooperative (k_walk2w): one warp per cut ray continues its
-// walk from the saved remainder with k_warp's ordered frontier — lane i holds
-// entry i of the ordered list of disjoint subtrees covering the rest of the
-// ray, every unresolved entry is expanded at once (up to 32 independent node
-// loads instead of one dependent chain per thread), the tail beyond 32 spills
-// to a per-warp LIFO — and appends the leading leaves to the ray's list up to
-// the list capacity, with the opacity-minorant stop of walk_step.  The listed
-// leaves are the same set in the same order as walk_step's, up to subtrees
-// whose conservative (float) bounds meet [t_min, t_max] but hold no
-// intersecting region: k_warp's exact slab test skips those either way.
-constexpr int kW2Stack = 256;  // spilled entries per warp
-#ifndef XB_WALK2W
-#define XB_WALK2W 1
-#endif
-__global__ void __launch_bounds__(kWarpThreads) k_walk2w(const __grid_constant__ RenderArgs A, int64_t n_slots) {
-    __shared__ SpillEnt s_stk[kWarpsPerBlock][kW2Stack];
-    __shared__ int s_code[kWarpsPerBlock][32];
-    __shared__ double s_tn[kWarpsPerBlock][32], s_tfar[kWarpsPerBlock][32];
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const SceneView& S = A.S;
-    SpillEnt* __restrict__ stk = s_stk[wid];
-    const int64_t n_cut = (int64_t)A.walk_counter[2];
-    const int64_t n_work = n_cut >= A.walk2_min ? n_cut : 0;
-    const int cap = A.leaf_cap;
-    const float spc = (float)A.M.spc;
-    for (;;) {
-        unsigned long long c = 0;
-        if (lane == 0) c = atomicAdd(A.walk_ctr, 1ull);
-        c = __shfl_sync(FULL, c, 0);
-        if ((int64_t)c >= n_work) break;
-        const int64_t slot = A.cut_list[c];
-        int32_t* res = A.resume + slot * (int64_t)(1 + 3 * kResume);
-        const int m0 = res[0];
-        if (m0 <= 0) continue;  // remainder not saved: k_warp restarts at the root
-        const SlotPix spx = slot_pixel(A, slot);
-        Ray r;
-        pixel_ray(A, spx.x, spx.y, r);
-        double tmin = 0.0, tmax = kTFar;
-        clip_ray(A.M, r, tmin, tmax);
-        if (A.M.iso_on && !A.walk_iso) tmax = A.iso_tend[slot];
-        int sg[3];
-        for (int q = 0; q < 3; q++) sg[q] = r.d[q] > 0.0 ? 1 : (r.d[q] < 0.0 ? -1 : 0);
-        // the saved remainder: entries 0..31 to the lanes, the rest to the stack (earliest on top)
-        int n = min(m0, 32), spn = 0;
-        int e_code = 0;
-        double e_tn = 0.0, e_tf = 0.0;
-        if (lane < n) {
-            e_code = res[1 + 3 * lane];
-            e_tn = (double)__int_as_float(res[2 + 3 * lane]);
-            e_tf = (double)__int_as_float(res[3 + 3 * lane]);
-        }
-        if (m0 > 32) {
-            spn = m0 - 32;
-            for (int q = lane; q < spn; q += 32) {
-                const int k = 32 + q;
-                stk[spn - 1 - q] = SpillEnt{res[1 + 3 * k], __int_as_float(res[2 + 3 * k]), __int_as_float(res[3 + 3 * k])};
-            }
-        }
-        __syncwarp();
-        const int lraw = A.leaf_count[slot];
-        int count = lraw & kLeafCountMask;
-        int flags = lraw & kLeafHeavy;
-        int32_t* __restrict__ out = A.leaves + slot * (int64_t)A.leaf_cap;
-        float tau = 0.f;
-        bool saved = false;  // truncated: the remainder (frontier from lane 0 + stack) goes to res
-        for (;;) {
-            if (n < 32 && spn > 0) {  // refill from the spill stack (earliest on top)
-                const int q = min(32 - n, spn);
-                if (lane >= n && lane < n + q) {
-                    const SpillEnt f = stk[spn - 1 - (lane - n)];
-                    e_code = f.code;
-                    e_tn = (double)f.tn;
-                    e_tf = (double)f.tf;
-                }
-                spn -= q;
-                n += q;
-                __syncwarp();
-            }
-            if (n == 0) break;  // walk complete
-            const unsigned leafm = __ballot_sync(FULL, lane < n && e_code <= -2);
-            const int nl = leafm == FULL ? 32 : __ffs(~leafm) - 1;
-            if (nl > 0) {
-                // append the leading leaves in order, up to the capacity and the minorant stop
-                if (count == cap) {  // a leaf beyond the capacity: truncated here (walk_step's rule)
-                    flags = kLeafTruncated;
-                    saved = true;
-                    break;
-                }
-                const int room = min(nl, cap - count);
-                float q = 0.f;
-                if (A.wqmin && lane < room) q = __ldg(A.wqmin + (-2 - e_code)) * (float)(e_tf - e_tn) * spc;
-                float qs = q;  // inclusive prefix of the minorant depth over the appended leaves
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const float v = __shfl_up_sync(FULL, qs, o);
-                    if (lane >= o) qs += v;
-                }
-                // the first leaf whose running depth passes the stop ends the walk after listing it
-                const unsigned stopm = A.wqmin ? __ballot_sync(FULL, lane < room && tau + qs > A.walk_tau_stop) : 0u;
-                const int take = stopm ? __ffs(stopm) : room;  // leaves listed now
-                if (lane < take) out[count + lane] = -2 - e_code;
-                count += take;
-                tau += __shfl_sync(FULL, qs, take - 1);
-                e_code = __shfl_down_sync(FULL, e_code, take);
-                e_tn = __shfl_down_sync(FULL, e_tn, take);
-                e_tf = __shfl_down_sync(FULL, e_tf, take);
-                n -= take;
-                if (stopm) {  // surely terminated: the rest is k_warp's if the ray goes on
-                    flags = kLeafTruncated | kLeafTauStop;
-                    saved = true;
-                    break;
-                }
-                continue;
-            }
-            // expansion step (k_warp's): every unresolved entry -> its surviving children, near first
-            bool actx = lane < n && e_code >= 0;
-            if (spn + 96 > kW2Stack) {  // near the spill limit: expand the first entry only
-                const unsigned um = __ballot_sync(FULL, actx);
-                actx = actx && lane == __ffs(um) - 1;
-            }
-            int oc[4] = {e_code, 0, 0, 0};
-            double otn[4] = {e_tn, 0.0, 0.0, 0.0}, otf[4] = {e_tf, 0.0, 0.0, 0.0};
-            bool ov[4] = {lane < n && !actx, false, false, false};
-            if (actx) {
-                const Kd4Node nd = S.kd4[e_code];
-                const uint32_t msk = A.wmask4[e_code];
-                int hs0 = 0, hs1 = 0, nh = 1;
-                double hn0 = e_tn, hf0 = e_tf, hn1 = 0.0, hf1 = 0.0;
-                {
-                    const int ax = nd.axes & 3;
-                    const double p = (double)nd.plane[0] * 0.5;
-                    const double oa = sel3(ax, r.o);
-                    const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
-                    if (sa == 0) {
-                        hs0 = oa < p ? 0 : 1;
-                    } else {
-                        const double tp = (p - oa) * sel3(ax, r.inv);
-                        const int ns_ = sa > 0 ? 0 : 1;
-                        if (tp >= e_tf) hs0 = ns_;
-                        else if (tp <= e_tn) hs0 = 1 - ns_;
-                        else { hs0 = ns_; hf0 = tp; hs1 = 1 - ns_; hn1 = tp; hf1 = e_tf; nh = 2; }
-                    }
-                }
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    if (h < nh) {
-                        const int sd = h ? hs1 : hs0;
-                        const double hn = h ? hn1 : hn0, hf = h ? hf1 : hf0;
-                        const int ax = (nd.axes >> (2 + 2 * sd)) & 3;
-                        int s0 = 2 * sd, s1 = -1;
-                        double a0 = hn, b0 = hf, a1 = 0.0, b1 = 0.0;
-                        if (ax != 3) {
-                            const double p = (double)(sd ? nd.plane[2] : nd.plane[1]) * 0.5;
-                            const double oa = sel3(ax, r.o);
-                            const int sa = ax == 0 ? sg[0] : (ax == 1 ? sg[1] : sg[2]);
-                            if (sa == 0) {
-                                s0 = 2 * sd + (oa < p ? 0 : 1);
-                            } else {
-                                const double tp = (p - oa) * sel3(ax, r.inv);
-                                const int nq = sa > 0 ? 0 : 1;
-                                if (tp >= b0) s0 = 2 * sd + nq;
-                                else if (tp <= a0) s0 = 2 * sd + 1 - nq;
-                                else { s0 = 2 * sd + nq; b0 = tp; s1 = 2 * sd + 1 - nq; a1 = tp; b1 = hf; }
-                            }
-                        }
-                        // cull as walk_step: inactive, or entirely outside [t_min, t_max]
-                        ov[2 * h] = ((msk >> s0) & 1) && b0 > tmin && a0 < tmax;
-                        oc[2 * h] = kd4_child(nd, s0); otn[2 * h] = a0; otf[2 * h] = b0;
-                        ov[2 * h + 1] = s1 >= 0 && ((msk >> s1) & 1) && b1 > tmin && a1 < tmax;
-                        oc[2 * h + 1] = kd4_child(nd, s1 < 0 ? 0 : s1); otn[2 * h + 1] = a1; otf[2 * h + 1] = b1;
-                    }
-                }
-            }
-            const int cnt = (int)ov[0] + (int)ov[1] + (int)ov[2] + (int)ov[3];
-            const unsigned m1 = __ballot_sync(FULL, cnt & 1), m2 = __ballot_sync(FULL, cnt & 2),
-                           m4 = __ballot_sync(FULL, cnt & 4);
-            const int pos = __popc(m1 & lt_mask) + 2 * __popc(m2 & lt_mask) + 4 * __popc(m4 & lt_mask);
-            const int total = __popc(m1) + 2 * __popc(m2) + 4 * __popc(m4);
-            if (spn + max(0, total - 32) > kW2Stack) __trap();  // cannot happen: see the guard above
-            int p = pos;
-#pragma unroll
-            for (int c2 = 0; c2 < 4; c2++) {
-                if (ov[c2]) {
-                    if (p < 32) {
-                        s_code[wid][p] = oc[c2];
-                        s_tn[wid][p] = otn[c2];
-                        s_tfar[wid][p] = otf[c2];
-                    } else {
-                        SpillEnt& f = stk[spn + (total - 1 - p)];
-                        f.code = oc[c2];
-                        f.tn = __double2float_rd(otn[c2]);
-                        f.tf = __double2float_ru(otf[c2]);
-                    }
-                    p++;
-                }
-            }
-            __syncwarp();
-            if (total > 32) spn += total - 32;
-            n = min(total, 32);
-            if (lane < n) {
-                e_code = s_code[wid][lane];
-                e_tn = s_tn[wid][lane];
-                e_tf = s_tfar[wid][lane];
-            }
-            __syncwarp();
-        }
-        if (saved) {  // the ordered remainder: frontier lanes 0..n-1, then the stack from the top
-            const int m = n + spn;
-            if (m > kResume) {
-                if (lane == 0) res[0] = -1;  // too long: k_warp restarts at the root (exact as well)
-            } else {
-                if (lane == 0) res[0] = m;
-                if (lane < n) {
-                    res[1 + 3 * lane] = e_code;
-                    res[2 + 3 * lane] = __float_as_int(__double2float_rd(e_tn));
-                    res[3 + 3 * lane] = __float_as_int(__double2float_ru(e_tf));
-                }
-                for (int q = lane; q < spn; q += 32) {
-                    const SpillEnt f = stk[spn - 1 - q];
-                    const int k = n + q;
-                    res[1 + 3 * k] = f.code;
-                    res[2 + 3 * k] = __float_as_int(f.tn);
-                    res[3 + 3 * k] = __float_as_int(f.tf);
-                }
-            }
-        }
-        if (lane == 0) A.leaf_count[slot] = count | flags;
-        __syncwarp();
-    }
-    (void)n_slots;
-}
-
 template <bool COUNT>
 __global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant__ RenderArgs A, int64_t n_slots) {
     const unsigned FULL = 0xffffffffu;
@@ -1849,22 +1615,8 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
             XB_CUDA(cudaLaunchKernel((const void*)k_route, dim3(grid_for(n_slots, kWalkThreads * kRouteSub)),
                                      dim3(kWalkThreads), wargs, 0, s));
             if (A.cut_list && A.walk_cap1 < A.leaf_cap)  // pass 2 over the cap-cut walks
-                if (XB_WALK2W) {  // warp-cooperative pass 2: one resident grid, warps grab cut rays
-                    static int grid2 = 0;
-                    if (!grid2) {
-                        int dev = 0, sms = 0, per_sm = 0;
-                        XB_CUDA(cudaGetDevice(&dev));
-                        XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-                        XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_walk2w,
-                                                                              kWarpThreads, 0));
-                        grid2 = std::max(1, sms * std::max(per_sm, 1));
-                    }
-                    XB_CUDA(cudaMemsetAsync(A.walk_ctr, 0, sizeof(unsigned long long), s));
-                    XB_CUDA(cudaLaunchKernel((const void*)k_walk2w, dim3(grid2), dim3(kWarpThreads), wargs, 0, s));
-                } else {
-                    XB_CUDA(cudaLaunchKernel((const void*)k_walk2, dim3(grid_for(n_slots, kWalkThreads)),
-                                             dim3(kWalkThreads), wargs, 0, s));
-                }
+                XB_CUDA(cudaLaunchKernel((const void*)k_walk2, dim3(grid_for(n_slots, kWalkThreads)),
+                                         dim3(kWalkThreads), wargs, 0, s));
             if (A.short_list && !A.fuse_short) {  // short rays -> k_short (when >= short_min of them)
                 using ShortFn = void (*)(RenderArgs, int64_t);
                 ShortFn sf;

@@ -52,7 +52,6 @@ struct RenderArgs {
     int32_t* resume;                   // per slot: k_walk's ordered remainder when truncated (1 + 3 x kResume words)
     const float* vqmin;                // per region opacity minorant (k_walk early stop), may be NULL
     unsigned long long* walk_counter;  // list lengths: [0] short, [1] long, [2] cut, [3] hit, [4] any
-    unsigned long long* walk_ctr;      // k_walk2w's ray counter
     int32_t* hit_list;                 // candidate rays (k_walk's work), appended by k_classify
     int32_t* long_list;                // rays for k_warp / k_iso_warp (k_route, in hit-list order)
     int32_t* any_list;                 // long + short rays, merged (k_warp's work when k_short is off)
