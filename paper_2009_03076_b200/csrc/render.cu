@@ -232,7 +232,10 @@ __device__ __forceinline__ void lattice(double ci, double co, double dt, double 
 // atomic — against these one-ray-per-thread kernels: orbit-mean C3 0.905 vs
 // 0.898 ms, C2 6.32 vs 6.04, C5 3.47 vs 3.34.  Refilled lanes lose the screen
 // coherence of a warp's 32 neighbouring rays, and the block scheduler already
-// balances the short blocks.)
+// balances the short blocks.  A warp-cooperative pass 2 — one warp per cut ray
+// continuing with k_warp's ordered frontier, 32 node loads in flight — lost as
+// well: C2 6.55 vs 6.05 ms, C5 3.91 vs 3.35 (commit 3643681, reverted): most
+// frontiers are narrow, so the warp's lanes idle in each expansion step.)
 // k_walk: the traversal half of the frame, one thread per ray.  Each thread
 // walks the Kd4 tree front to back with a private stack and lists the active
 // leaf regions its ray meets, in r_in order, culled only by [t_min, t_max]
