@@ -572,6 +572,32 @@ def frame_parity(S, bands):
             "ok": d <= RGBA_TOL and bad_r == 0 and bad_s == 0}
 
 
+def oracle_parity(S, seconds, view=0, osc=None):
+    """Oracle row bands (~`seconds` of host work) of an orbit view against the GPU
+    float frame: the in-run frame parity of the secondary / extra configs (`osc`:
+    an oracle scene of the same model to reuse)."""
+    import oracle
+
+    if osc is None:
+        osc = oracle.OracleScene({k: getattr(S.model, k) for k in MODEL_KEYS},
+                                 {k: getattr(S.regions, k) for k in REGION_KEYS})
+    cam = S.cams[view]
+    _, _, _, bands = cpu_bands(osc, cam, S.tf, S.params, seconds, os.cpu_count() or 1, iso=S.cfg.get("iso"))
+    from paper_2009_03076_b200.render import render_frame_float
+
+    u8, f64, cnt, st = render_frame_float(S.scene, cam, S.tf, S.params)
+    f, c = f64.reshape(-1, 4), cnt.reshape(-1, 2)
+    d, bad_r, bad_s, px = 0.0, 0, 0, 0
+    for b, e, of, pr, ps in bands:
+        d = max(d, float(np.abs(f[b:e] - of).max()))
+        bad_r += int(np.count_nonzero(c[b:e, 0] != pr))
+        bad_s += int(np.count_nonzero(c[b:e, 1] != ps))
+        px += e - b
+    return {"view": view, "pixels": px, "max_abs_drgba": d, "tolerance": RGBA_TOL,
+            "px_region_counter_mismatches": bad_r, "px_sample_counter_mismatches": bad_s,
+            "ok": d <= RGBA_TOL and bad_r == 0 and bad_s == 0}
+
+
 def e2e_orbit(S, steps):
     """The public API with host output, cycling the orbit: `render_frames` (the
     host copy of frame k overlaps the march of frame k+1; wall time over the K
@@ -736,7 +762,7 @@ def bench_ours(args):
                                                          "equal to the oracle's own by the builder parity)",
                                         "msamples_per_s": ms_, **host_info()}
                 line["parity"]["frame"] = frame_parity(S, bands)
-                del osc
+                S.osc = osc  # reused by C4's frame parity (same model)
             else:
                 line["cpu_baseline"] = None
             pb = line["parity"]["builders"]
@@ -752,6 +778,10 @@ def bench_ours(args):
             if full:
                 line["secondary"]["parity"] = {"builders": S2.builder_parity()}
                 ok = ok and (line["secondary"]["parity"]["builders"] or {"equal": True})["equal"]
+                if world == 1 and not args.no_cpu_baseline:
+                    fp = oracle_parity(S2, 3.0)
+                    line["secondary"]["parity"]["frame"] = fp
+                    ok = ok and fp["ok"]
         if full and not args.no_ablations and world == 1:
             from paper_2009_03076_b200.bricks import BrickBuildParams, build_bricks
 
@@ -771,10 +801,18 @@ def bench_ours(args):
             if rank == 0:
                 line_extra[name] = dict(rx, config=workload_config(cfg_x, args.views, Sx.n_cells, Sx.model.n_bricks,
                                                                    len(Sx.regions)), build_ms=Sx.build_ms)
+                line_extra[name]["parity"] = {}
                 if Sx.build_ms and "bricks" in Sx.build_ms:  # a model of its own: its builder parity
                     pb = Sx.builder_parity()
-                    line_extra[name]["parity"] = {"builders": pb}
+                    line_extra[name]["parity"]["builders"] = pb
                     ok = ok and (pb or {"equal": True})["equal"]
+                reuse = getattr(S, "osc", None) if Sx.model is S.model else None
+                if world == 1 and not args.no_cpu_baseline and (reuse is not None or Sx.n_cells < 300_000_000):
+                    fp = oracle_parity(Sx, 3.0, osc=reuse)
+                    line_extra[name]["parity"]["frame"] = fp
+                    ok = ok and fp["ok"]
+                elif world == 1:  # C5: the oracle's BVH over 50M regions takes minutes; builders by digests
+                    line_extra[name]["parity"]["frame"] = "not run in the bench (oracle scene build too slow)"
             del Sx
             torch.cuda.empty_cache()
         if rank == 0:

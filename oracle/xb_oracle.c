@@ -482,6 +482,16 @@ XO_API double xo_max_opacity(double lo, double hi, const double* rgba, double vm
     return m;
 }
 
+/* the volume active set over every region (build_volume_bvh's filter, R/accel.py:227-234):
+ * ids with max_opacity(tf, vr[r]) > 0, ascending; returns their count */
+XO_API int64_t xo_active_volume(double lo, double hi, const double* rgba, int64_t n, const double* vr, int64_t stride,
+                                int64_t* out) {
+    int64_t k = 0;
+    for (int64_t r = 0; r < n; r++)
+        if (xo_max_opacity(lo, hi, rgba, vr[r * stride], vr[r * stride + 1]) > 0.0) out[k++] = r;
+    return k;
+}
+
 static inline void tf_eval(double tf_lo, double tf_hi, const double* rgba, double v, double out[4]) {
     double t = (v - tf_lo) / (tf_hi - tf_lo);
     if (t < 0.0) t = 0.0;
