@@ -182,6 +182,56 @@ def make_cells(cfg, host=False):
     return xio.generate_synthetic(spec, workers=os.cpu_count() or 1)
 
 
+def coll(fn, t, **kw):
+    """A torch.distributed collective on tensor `t` in place: NCCL moves device
+    memory directly; gloo (the shared-GPU check of the N > 1 path) goes through
+    the host."""
+    import torch.distributed as dist
+
+    if t.is_cuda and dist.get_backend() == "gloo":
+        c = t.cpu()
+        fn(c, **kw)
+        t.copy_(c)
+    else:
+        fn(t, **kw)
+
+
+def make_cells_ranks(cfg, rank, world, dev):
+    """The config's cells on every rank: generated once on rank 0 (the numpy
+    generator, bit-exact to the reference's) and broadcast over NCCL into
+    device-resident cells on each rank (8 host-side generations would need
+    8 x 21 GB of host memory at C3)."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2009_03076_b200 import _native as N
+    from paper_2009_03076_b200 import io as xio
+
+    if world == 1:
+        return make_cells(cfg)
+    cl = make_cells(cfg) if rank == 0 else None
+    n_t = torch.tensor([len(cl) if cl is not None else 0], dtype=torch.int64, device=dev)
+    coll(dist.broadcast, n_t, src=0)
+    n = int(n_t.item())
+    cols = []
+    for name, dt in (("i", torch.int32), ("j", torch.int32), ("k", torch.int32), ("level", torch.int32),
+                     ("values", torch.float32)):
+        t = torch.empty(n, dtype=dt, device=dev)
+        if rank == 0:
+            a = getattr(cl, name)
+            t.copy_(torch.from_numpy(np.ascontiguousarray(a[:, 0] if name == "values" else a)))
+        coll(dist.broadcast, t, src=0)
+        cols.append(t)
+    torch.cuda.synchronize()
+    h = N.new_handle()
+    N.check(N.lib().xb_cells_create(n, dev.index, C.byref(h)))
+    ch = N.CellsHandle(h.value, dev.index)
+    N.check(N.lib().xb_cells_upload(ch.h, 0, n, *(N.ptr(t.data_ptr()) for t in cols)))
+    return xio.DeviceCells(ch, n, spec_for(cfg).field_name)
+
+
 def cameras_for(bounds, cfg, n_views):
     from paper_2009_03076_b200.orbit import orbit_cameras
 
@@ -388,7 +438,7 @@ def bench_reference(args, cfg):
 class Scene:
     """A built config on this rank: model, regions, active sets, cameras."""
 
-    def __init__(self, cfg, name, n_views, build_reps=3, cells=None, model=None, regions=None):
+    def __init__(self, cfg, name, n_views, build_reps=3, cells=None, model=None, regions=None, dist_ctx=None):
         import torch
 
         from paper_2009_03076_b200.bricks import build_bricks
@@ -397,7 +447,8 @@ class Scene:
 
         self.cfg, self.name = cfg, name
         if model is None:
-            cells = make_cells(cfg) if cells is None else cells
+            if cells is None:
+                cells = make_cells_ranks(cfg, *dist_ctx) if dist_ctx else make_cells(cfg)
             self.n_cells = len(cells)
             # build timings: one untimed warm-up build (device pool, page-locked staging), then the
             # median of `build_reps` builds
@@ -492,7 +543,7 @@ def time_frames(S, args, steps, warmup, world, rank, dev, with_clocks=False):
     march_ms = mt if len(mt) == steps else np.full(steps, np.nan)
     if world > 1:  # max over ranks, per step
         t = torch.tensor(np.stack([frame_ms, march_ms]), dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        coll(dist.all_reduce, t, op=dist.ReduceOp.MAX)
         frame_ms, march_ms = t.cpu().numpy()
     return frame_ms, march_ms, (sampler.summary() if sampler else None), rend
 
@@ -517,7 +568,7 @@ def count_views(S, world, rank, dev):
     torch.cuda.synchronize()
     t = torch.tensor(rows, dtype=torch.int64, device=dev)
     if world > 1:
-        dist.all_reduce(t)
+        coll(dist.all_reduce, t)
     return t.cpu().numpy()
 
 
@@ -674,13 +725,21 @@ def bench_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # XB_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 over gloo, to run the
+    # N > 1 code path on a one-GPU box (NCCL refuses two ranks on one device)
+    shared = os.environ.get("XB_BENCH_SHARE_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nccl = None
-    if world > 1:
+    if world > 1 and shared:
+        dist.init_process_group("gloo")
+    elif world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if world > 1:
         x = torch.ones(1, device=dev)
-        dist.all_reduce(x)  # communicator up; its size must equal the world
+        coll(dist.all_reduce, x)  # communicator up; its size must equal the world
         nccl = {"backend": dist.get_backend(), "world": dist.get_world_size(), "allreduce_ones": int(x.item()),
                 "version": ".".join(map(str, torch.cuda.nccl.version()))}
         if nccl["allreduce_ones"] != world:
@@ -695,7 +754,8 @@ def bench_ours(args):
         peaks = json.loads(pk.read_text())
     cfg = CONFIGS[args.config]
     full = not args.profile
-    S = Scene(cfg, args.config, args.views, build_reps=3 if full else 0)
+    dctx = (rank, world, dev) if world > 1 else None
+    S = Scene(cfg, args.config, args.views, build_reps=3 if full else 0, dist_ctx=dctx)
     res, clocks, rend = run_config(args, S, world, rank, dev, peaks, args.steps, args.warmup, with_clocks=full)
     line = None
     ok = True
@@ -770,7 +830,7 @@ def bench_ours(args):
             line["parity"]["ok"] = ok
     # secondary and extra configs
     if args.secondary and args.secondary != args.config:
-        S2 = Scene(CONFIGS[args.secondary], args.secondary, args.views, build_reps=1 if full else 0)
+        S2 = Scene(CONFIGS[args.secondary], args.secondary, args.views, build_reps=1 if full else 0, dist_ctx=dctx)
         r2, _, _ = run_config(args, S2, world, rank, dev, peaks, 8, 4)
         if rank == 0:
             line["secondary"] = dict(r2, config=workload_config(S2.cfg, args.views, S2.n_cells, S2.model.n_bricks,
@@ -796,7 +856,7 @@ def bench_ours(args):
                 Sx = Scene(cfg_x, name, args.views, cells=S.n_cells, model=S.model, regions=S.regions)
                 Sx.build_ms = tf_refresh(Sx)
             else:
-                Sx = Scene(cfg_x, name, args.views, build_reps=1)
+                Sx = Scene(cfg_x, name, args.views, build_reps=1, dist_ctx=dctx)
             rx, _, _ = run_config(args, Sx, world, rank, dev, peaks, 8, 4)
             if rank == 0:
                 line_extra[name] = dict(rx, config=workload_config(cfg_x, args.views, Sx.n_cells, Sx.model.n_bricks,
@@ -875,7 +935,7 @@ def e2e_tiled(S, rend, steps, world, rank, dev):
         torch.cuda.synchronize()
     te = time.perf_counter() - te
     tt = torch.tensor([te], dtype=torch.float64, device=dev)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    coll(dist.all_reduce, tt, op=dist.ReduceOp.MAX)
     return float(tt.item()) / steps * 1000.0
 
 

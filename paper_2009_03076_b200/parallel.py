@@ -108,16 +108,31 @@ class TiledRenderer:
             raise ValueError(f"camera is {camera.width}x{camera.height} but the renderer was built for "
                              f"{self.width}x{self.height}")
 
+    def _staged(self):
+        # gloo moves host memory: device buffers go through the host (CPU tests,
+        # bench.py's shared-GPU check of the N > 1 path); NCCL moves them directly
+        return self.packed.is_cuda and self.dist.get_backend(self.group) == "gloo"
+
     def exchange(self):
         """All-gather every rank's packed tiles into `gathered` (rank-major)."""
         if self.world > 1:
-            self.dist.all_gather_into_tensor(self.gathered, self.packed, group=self.group)
+            if self._staged():
+                out = self.torch.empty(self.gathered.shape, dtype=self.gathered.dtype)
+                self.dist.all_gather_into_tensor(out, self.packed.cpu(), group=self.group)
+                self.gathered.copy_(out)
+            else:
+                self.dist.all_gather_into_tensor(self.gathered, self.packed, group=self.group)
         return self.gathered
 
     def reduce_counters(self):
         """Sum [regions, samples, bytes] over the ranks (one all-reduce)."""
         if self.world > 1:
-            self.dist.all_reduce(self.counters, group=self.group)
+            if self._staged():
+                c = self.counters.cpu()
+                self.dist.all_reduce(c, group=self.group)
+                self.counters.copy_(c)
+            else:
+                self.dist.all_reduce(self.counters, group=self.group)
         return self.counters
 
     def assemble(self, stream=None):

@@ -67,3 +67,24 @@ def test_reference_arm_loads_no_gpu_library():
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "LIB False" in out.stdout
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu():
+    """The N > 1 path of bench.py end to end on a one-GPU box: `--gpus 2`
+    relaunches under torch.distributed.run, both ranks share cuda:0 over gloo
+    (XB_BENCH_SHARE_GPU=1; NCCL refuses two ranks on one device), cells are
+    broadcast from rank 0, tiles rendered per rank, gathered, unpacked and the
+    counters all-reduced: the frame counters equal the one-rank run's."""
+    env = dict(os.environ, XB_BENCH_SHARE_GPU="1")
+    args = ["--config", "c1", "--secondary", "", "--extra", "", "--steps", "2", "--warmup", "1"]
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", *args], capture_output=True,
+                         text=True, cwd=ROOT, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d2 = json.loads(lines[0])
+    d1 = _run(*args, "--no-cpu-baseline")
+    assert d2["n_gpus"] == 2 and d2["nccl"]["world"] == 2 and d2["value"] > 0
+    assert d2["frame"] == d1["frame"]  # counters of the tiled frame, summed over the ranks
+    assert d2["e2e"]["value"] > 0
