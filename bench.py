@@ -614,7 +614,8 @@ def frame_parity(S, bands):
     c = cnt.reshape(-1, 2)
     d, bad_r, bad_s, px = 0.0, 0, 0, 0
     for b, e, of, pr, ps in bands:
-        d = max(d, float(np.abs(f[b:e] - of).max()))
+        dd = np.abs(f[b:e] - of)
+        d = max(d, float(dd.max()) if np.isfinite(dd).all() else float("inf"))  # NaN / inf fail
         bad_r += int(np.count_nonzero(c[b:e, 0] != pr))
         bad_s += int(np.count_nonzero(c[b:e, 1] != ps))
         px += e - b
@@ -640,7 +641,8 @@ def oracle_parity(S, seconds, view=0, osc=None):
     f, c = f64.reshape(-1, 4), cnt.reshape(-1, 2)
     d, bad_r, bad_s, px = 0.0, 0, 0, 0
     for b, e, of, pr, ps in bands:
-        d = max(d, float(np.abs(f[b:e] - of).max()))
+        dd = np.abs(f[b:e] - of)
+        d = max(d, float(dd.max()) if np.isfinite(dd).all() else float("inf"))  # NaN / inf fail
         bad_r += int(np.count_nonzero(c[b:e, 0] != pr))
         bad_s += int(np.count_nonzero(c[b:e, 1] != ps))
         px += e - b

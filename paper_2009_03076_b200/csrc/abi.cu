@@ -851,7 +851,15 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             XB_CUDA(cudaEventCreate(&me.ev[1]));
             A->march_events = me.ev;
         }
+        int32_t* fixup_buf = nullptr;  // k_warp's pixels for the exact FP64 shading re-render (k_fixup)
+        if (A->kernel == 0 && A->M.grad_mode == 1) {
+            const size_t n_slots = std::max<size_t>((size_t)n_local * xb::kTileW * xb::kTileH, 1);
+            XB_CUDA(cudaMallocAsync((void**)&fixup_buf, n_slots * sizeof(int32_t), s));
+            A->fixup_list = fixup_buf;
+            A->fixup_count = scratch + 19;
+        }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
+        if (fixup_buf) XB_CUDA(cudaFreeAsync(fixup_buf, s));
         if (A->march_events) {
             std::lock_guard<std::mutex> eg(g_events_mu);
             g_events.push_back(me);

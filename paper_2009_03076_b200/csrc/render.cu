@@ -767,6 +767,7 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
     const int32_t* __restrict__ list = A.leaves + slot * (int64_t)A.leaf_cap;
     double ar = 0.0, ag = 0.0, ab = 0.0, aa = 0.0;
     int nreg = 0, nsmp = 0;
+    bool fix = false;
     double t = tmin;
     for (int li = 0; li < count && aa < A.M.early; li++) {
         const int rid = list[li];
@@ -804,6 +805,7 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
                         double f;
                         if (GRAD == 1) {
                             f = shade_factor_f(F.g, r);
+                            if (f < 0.0) { f = 0.2; fix = true; }  // exact FP64 re-render (k_fixup)
                         } else {
                             double g[3];
                             int64_t ne = 0;
@@ -836,6 +838,7 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
         }
     }
     write_pixel(A, sp.out, acc, nreg, nsmp);
+    if (fix && A.fixup_list) A.fixup_list[atomicAdd(A.fixup_count, 1ull)] = (int32_t)slot;
     my_reg += nreg;
     my_smp += nsmp;
 }
@@ -964,6 +967,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             const int64_t out_px = q.out;
             double Tr = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;  // transmittance, premultiplied colour
             int nreg = 0, nsmp = 0;
+            bool fix = false;  // a sample's FP32 gradient was untrusted (shade_factor_f)
             {
                 RayAxes& rs = s_ray[wid];
                 __syncwarp();
@@ -1068,6 +1072,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                                         double f;
                                         if (GRAD == 1) {
                                             f = shade_factor_f(F.g, r);
+                                            if (f < 0.0) { f = 0.2; fix = true; }  // exact re-render (k_fixup)
                                         } else {
                                             double g[3];
                                             int64_t ne = 0;
@@ -1422,6 +1427,10 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                     }
                 }
                 write_pixel(A, out_px, acc, nreg, nsmp);
+            }
+            if (__any_sync(FULL, fix) && lane == 0 && A.fixup_list)
+                A.fixup_list[atomicAdd(A.fixup_count, 1ull)] = (int32_t)slot;
+            if (lane == 0) {
                 if (kDebugChunks && A.dbg) {
                     atomicAdd(A.dbg + 2, 1ull);
                     atomicAdd(A.dbg + 3, (unsigned long long)nsmp);
@@ -1454,6 +1463,45 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
         atomicAdd(&A.stats[0], tot_reg);
         atomicAdd(&A.stats[1], tot_smp);
         if (COUNT) atomicAdd(&A.stats[2], tot_bytes);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_fixup: pixels whose FP32 shading gradient was untrusted (shade_factor_f)
+// are re-rendered one thread each with the exact per-pixel path — the
+// reference's FP64 gradient sums (volume_ray) — after k_warp.  The counters
+// are the same as k_warp's, so the frame stats are not touched.
+
+template <bool ISO>
+__global__ void __launch_bounds__(128) k_fixup(const __grid_constant__ RenderArgs A) {
+    __shared__ double s_tf[1024];
+    const int64_t n = (int64_t)*A.fixup_count;
+    if (blockIdx.x * (int64_t)blockDim.x >= n) return;
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
+    __syncthreads();
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slot = A.fixup_list[q];
+        const SlotPix sp = slot_pixel(A, slot);
+        RayStats st = {0, 0, 0};
+        Ray r;
+        pixel_ray(A, sp.x, sp.y, r);
+        const double rho = rho_hash((uint64_t)sp.pix, A.M.seed);
+        double tmin = 0.0, tmax = kTFar;
+        clip_ray(A.M, r, tmin, tmax);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (tmin < tmax) {
+            const double t_end = ISO ? A.iso_tend[slot] : tmax;
+            volume_ray<1, false>(A.S, A.vflags, A.M, s_tf, r, tmin, t_end, rho, acc, st, nullptr);
+            if (ISO && A.iso_shade[slot] >= 0.0) {
+                const double f = A.iso_shade[slot];
+                const double w = 1.0 - acc[3];
+                acc[0] += w * A.M.iso_rgb[0] * f;
+                acc[1] += w * A.M.iso_rgb[1] * f;
+                acc[2] += w * A.M.iso_rgb[2] * f;
+                acc[3] = 1.0;
+            }
+        }
+        write_pixel(A, sp.out, acc, (int)st.regions, (int)st.samples);
     }
 }
 
@@ -1647,11 +1695,17 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
     const int64_t want = (n_slots * 32 + threads - 1) / threads;  // k_warp: one ray per warp at a time
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), want));
     void* args[] = {(void*)&A, (void*)&n_slots};
+    if (A.fixup_list) XB_CUDA(cudaMemsetAsync(A.fixup_count, 0, sizeof(unsigned long long), s));
     cudaEvent_t* ev = (cudaEvent_t*)A.march_events;
     NvtxRange r_march("march: k_warp");
     if (ev) XB_CUDA(cudaEventRecord(ev[0], s));
     XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(threads), args, dyn, s));
     if (ev) XB_CUDA(cudaEventRecord(ev[1], s));
+    if (A.fixup_list && g == 1 && !count) {  // untrusted FP32 gradients: exact re-render of those pixels
+        void* fargs[] = {(void*)&A};
+        const void* ff = iso ? (const void*)k_fixup<true> : (const void*)k_fixup<false>;
+        XB_CUDA(cudaLaunchKernel(ff, dim3((unsigned)sms), dim3(128), fargs, 0, s));
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -58,6 +58,8 @@ struct RenderArgs {
     unsigned long long* dbg;           // diagnostics (XB_DEBUG_CHUNKS): k_warp chunks, chunk lanes, rays, samples
     int fuse_short;                    // k_warp runs the short rays after the long ones (no k_short launch)
     unsigned long long* short_counter; // k_warp's short-ray grab counter
+    int32_t* fixup_list;               // pixels for k_fixup (exact FP64 shading), or NULL
+    unsigned long long* fixup_count;
     int cut_tau;                       // k_walk2 also continues walks stopped by the opacity minorant
     int32_t* blk_counts;               // k_walk -> k_route: short / long / cut rays per k_walk block
     int32_t* short_list;               // rays with a complete list of <= 8 leaves (k_short's work), or NULL
