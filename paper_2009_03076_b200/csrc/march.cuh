@@ -735,15 +735,18 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, in
     if (GRAD) A.gradient(F.g);
 }
 
-// _shade_factor (R/render.py:284-289) on an unnormalised FP32 gradient direction.
-// Returns -1 when the FP32 gradient cannot be trusted: its largest component
-// below 2^-100 (in the far tail of a field the values are FP32 subnormals, the
-// partials lose their precision and 1/m overflows) or not finite.  A zero FP32
-// gradient is ambiguous (a constant field, or underflow) and counts as such
-// too.  The frame kernels then shade with 0.2 and list the pixel for
-// k_fixup, which re-renders it with the reference's exact FP64 gradient.
-__device__ __forceinline__ double shade_factor_f(const float g[3], const Ray& r) {
+// _shade_factor (R/render.py:284-289) on an unnormalised FP32 gradient direction
+// at a sample of value v.  Returns -1 when the FP32 gradient cannot be
+// trusted: its largest component below 2^-100 (in the far tail of a field the
+// values are FP32 subnormals: the partials lose their precision and 1/m
+// overflows) or not finite.  An exactly zero gradient at a value of normal
+// magnitude is genuine — every v - v0 is exactly 0 (a locally constant field,
+// or a single contributing cell) — and shades 0.2 like the reference.  On -1
+// the frame kernels shade with 0.2 and list the pixel for k_fixup, which
+// re-renders it with the reference's exact FP64 gradient.
+__device__ __forceinline__ double shade_factor_f(const float g[3], const Ray& r, double v) {
     const float m = fmaxf(fabsf(g[0]), fmaxf(fabsf(g[1]), fabsf(g[2])));
+    if (m == 0.f && fabs(v) >= 0x1p-60) return 0.2;
     if (!(m >= 0x1p-100f) || !(m < INFINITY)) return -1.0;
     const float s = 1.f / m;  // scale to [1, 3] before squaring: no under/overflow
     const float a = g[0] * s, b = g[1] * s, c = g[2] * s;

@@ -804,7 +804,7 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
                     if (GRAD != 0) {
                         double f;
                         if (GRAD == 1) {
-                            f = shade_factor_f(F.g, r);
+                            f = shade_factor_f(F.g, r, v);
                             if (f < 0.0) { f = 0.2; fix = true; }  // exact FP64 re-render (k_fixup)
                         } else {
                             double g[3];
@@ -1071,7 +1071,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                                     if (GRAD != 0) {
                                         double f;
                                         if (GRAD == 1) {
-                                            f = shade_factor_f(F.g, r);
+                                            f = shade_factor_f(F.g, r, v);
                                             if (f < 0.0) { f = 0.2; fix = true; }  // exact re-render (k_fixup)
                                         } else {
                                             double g[3];
