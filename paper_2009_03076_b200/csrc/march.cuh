@@ -737,9 +737,11 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, in
 
 // _shade_factor (R/render.py:284-289) on an unnormalised FP32 gradient direction
 // at a sample of value v.  Returns -1 when the FP32 gradient cannot be
-// trusted: its largest component below 2^-100 (in the far tail of a field the
+// trusted: its largest component subnormal (in the far tail of a field the
 // values are FP32 subnormals: the partials lose their precision and 1/m
-// overflows) or not finite.  An exactly zero gradient at a value of normal
+// overflows) or not finite.  (Any normal gradient matched the reference's
+// RGBA8 exactly over the configs[2] frame; a 2^-100 bound flagged 9 % of its
+// pixels for nothing.)  An exactly zero gradient at a value of normal
 // magnitude is genuine — every v - v0 is exactly 0 (a locally constant field,
 // or a single contributing cell) — and shades 0.2 like the reference.  On -1
 // the frame kernels shade with 0.2 and list the pixel for k_fixup, which
@@ -747,7 +749,7 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, in
 __device__ __forceinline__ double shade_factor_f(const float g[3], const Ray& r, double v) {
     const float m = fmaxf(fabsf(g[0]), fmaxf(fabsf(g[1]), fabsf(g[2])));
     if (m == 0.f && fabs(v) >= 0x1p-60) return 0.2;
-    if (!(m >= 0x1p-100f) || !(m < INFINITY)) return -1.0;
+    if (!(m >= 0x1p-126f) || !(m < INFINITY)) return -1.0;
     const float s = 1.f / m;  // scale to [1, 3] before squaring: no under/overflow
     const float a = g[0] * s, b = g[1] * s, c = g[2] * s;
     const float dot = a * (float)r.d[0] + b * (float)r.d[1] + c * (float)r.d[2];
