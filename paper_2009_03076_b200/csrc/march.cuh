@@ -744,8 +744,12 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, in
 // pixels for nothing.)  An exactly zero gradient at a value of normal
 // magnitude is genuine — every v - v0 is exactly 0 (a locally constant field,
 // or a single contributing cell) — and shades 0.2 like the reference.  On -1
-// the frame kernels shade with 0.2 and list the pixel for k_fixup, which
-// re-renders it with the reference's exact FP64 gradient.
+// the frame kernels shade with 0.2, and when the sample's opacity is not
+// negligible (>= kNegligibleAlpha: a shading error of at most 0.8 alpha could
+// show) list the pixel for k_fixup, which re-renders it with the reference's
+// exact FP64 gradient.  Subnormal values under a TF that maps them to an
+// alpha ~1e-38 (configs[2]'s far field) never need the re-render.
+constexpr double kNegligibleAlpha = 0x1p-40;
 __device__ __forceinline__ double shade_factor_f(const float g[3], const Ray& r, double v) {
     const float m = fmaxf(fabsf(g[0]), fmaxf(fabsf(g[1]), fabsf(g[2])));
     if (m == 0.f && fabs(v) >= 0x1p-60) return 0.2;

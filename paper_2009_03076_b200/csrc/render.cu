@@ -805,7 +805,10 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
                         double f;
                         if (GRAD == 1) {
                             f = shade_factor_f(F.g, r, v);
-                            if (f < 0.0) { f = 0.2; fix = true; }  // exact FP64 re-render (k_fixup)
+                            if (f < 0.0) {  // untrusted FP32 gradient (kNegligibleAlpha: see shade_factor_f)
+                                fix = fix || alpha >= kNegligibleAlpha;
+                                f = 0.2;
+                            }
                         } else {
                             double g[3];
                             int64_t ne = 0;
@@ -1072,7 +1075,10 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                                         double f;
                                         if (GRAD == 1) {
                                             f = shade_factor_f(F.g, r, v);
-                                            if (f < 0.0) { f = 0.2; fix = true; }  // exact re-render (k_fixup)
+                                            if (f < 0.0) {  // untrusted FP32 gradient (see shade_factor_f)
+                                                fix = fix || alpha >= kNegligibleAlpha;
+                                                f = 0.2;
+                                            }
                                         } else {
                                             double g[3];
                                             int64_t ne = 0;

@@ -203,9 +203,12 @@ def test_c3_builders_match_oracle_digests():
 
 def test_far_field_subnormal_values_shade_exactly():
     """A narrow gaussian whose tail values are FP32 subnormals: the FP32 shading
-    gradient of those samples underflows, so the frame kernel defers them to the
-    exact FP64 re-render (k_fixup) — no NaN, the oracle's frame within 1e-3,
-    counters equal (found against the reference's own renderer at configs[2])."""
+    gradient of those samples underflows (it produced NaN colours before round 2's
+    fix, found against the reference's own renderer at configs[2]).  Under the
+    data-range TF their opacity is negligible and they shade 0.2; under a TF
+    whose domain is the subnormal range itself they are opaque and the frame
+    kernel defers them to the exact FP64 re-render (k_fixup).  Either way: no
+    NaN, the oracle's frame within 1e-3, counters equal."""
     from paper_2009_03076_b200 import io as xio
     from paper_2009_03076_b200.orbit import orbit_cameras
     from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame, render_frame_float
@@ -217,7 +220,17 @@ def test_far_field_subnormal_values_shade_exactly():
     v = cells.values[:, 0]
     assert np.count_nonzero((v > 0) & (v < np.finfo(np.float32).tiny)) > 0  # subnormal tail present
     model, regions = _build(cells)
-    tf = bench.tf_for(model.value_range(0), dict(max_alpha=0.5))
+    from paper_2009_03076_b200.accel import TransferFunction
+
+    for tf in (bench.tf_for(model.value_range(0), dict(max_alpha=0.5)),
+               TransferFunction.grayscale((0.0, 2e-38), max_alpha=0.5)):
+        _subnormal_frames(model, regions, tf)
+
+
+def _subnormal_frames(model, regions, tf):
+    from paper_2009_03076_b200.orbit import orbit_cameras
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame, render_frame_float
+
     scene = build_scene(model, regions, tf)
     osc = _oracle_scene(model, regions)
     osc.set_tf(tf.domain, tf.rgba)
@@ -230,3 +243,56 @@ def test_far_field_subnormal_values_shade_exactly():
         assert np.array_equal(cnt[..., 0].ravel(), pr) and np.array_equal(cnt[..., 1].ravel(), ps)
         fr = render_frame(scene, cam, tf, params)
         assert np.abs(fr.rgba.astype(int) - ou.astype(int)).max() <= 1
+
+
+def test_reference_renderer_pixel_identical_c1():
+    """The installed reference itself (baseline/_ref: amrvol, numba) against the
+    GPU path at configs[0]: the reference's own builders give the same arrays,
+    and its render_frame the same RGBA8 frame and stats (two orbit views, one
+    with the iso-surface).  Skipped where the reference is not installed."""
+    import os
+    import sys
+
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "amrvol").exists():
+        pytest.skip("reference not installed in baseline/_ref")
+    try:
+        import numba  # noqa: F401
+    except ImportError:
+        pytest.skip("numba missing")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_ref")
+    sys.path.insert(0, str(ref))
+    from amrvol.accel import TransferFunction as RTF
+    from amrvol.bricks import build_bricks as r_build_bricks
+    from amrvol.model import CellList as RCells
+    from amrvol.regions import build_regions as r_build_regions
+    from amrvol.render import Camera as RCam
+    from amrvol.render import MarchParams as RParams
+    from amrvol.render import build_scene as r_build_scene
+    from amrvol.render import render_frame as r_render_frame
+
+    from paper_2009_03076_b200.render import MarchParams, build_scene, render_frame
+
+    bench = _bench()
+    cfg = bench.CONFIGS["c1"]
+    cells = bench.make_cells(cfg)
+    model, regions = _build(cells)
+    rm, _ = r_build_bricks(RCells(cells.i, cells.j, cells.k, cells.level, cells.values, cells.field_names))
+    rr = r_build_regions(rm)
+    for k in MODEL_KEYS:
+        assert np.array_equal(getattr(model, k), getattr(rm, k)), k
+    for k in REGION_KEYS:
+        assert np.array_equal(getattr(regions, k), getattr(rr, k)), k
+    tf = bench.tf_for(model.value_range(0), cfg)
+    rtf = RTF(tf.domain, tf.rgba)
+    lo, hi = model.value_range(0)
+    for view, iso in ((0, None), (3, 0.5 * (lo + hi))):
+        cam = bench.cameras_for(regions.bounds, cfg, 8)[view]
+        ours = render_frame(build_scene(model, regions, tf, iso_value=iso), cam, tf,
+                            MarchParams(seed=0, gradient_mode="analytic"))
+        rcam = RCam(cam.position, cam.forward, cam.up, cam.fov_y, cam.width, cam.height)
+        theirs = r_render_frame(r_build_scene(rm, rr, rtf, iso_value=iso), rcam, rtf,
+                                RParams(seed=0, gradient_mode="analytic"))
+        assert (ours.stats.regions, ours.stats.samples) == (theirs.stats.regions, theirs.stats.samples)
+        assert np.abs(ours.rgba.astype(int) - theirs.rgba.astype(int)).max() <= 1
+        assert np.count_nonzero(ours.rgba != theirs.rgba) <= ours.rgba.size // 10000
