@@ -856,7 +856,7 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             const size_t n_slots = std::max<size_t>((size_t)n_local * xb::kTileW * xb::kTileH, 1);
             XB_CUDA(cudaMallocAsync((void**)&fixup_buf, n_slots * sizeof(int32_t), s));
             A->fixup_list = fixup_buf;
-            A->fixup_count = scratch + 19;
+            A->fixup_count = scratch + 19;  // zeroed with the scratch
         }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
         if (fixup_buf) XB_CUDA(cudaFreeAsync(fixup_buf, s));

@@ -1701,7 +1701,6 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
     const int64_t want = (n_slots * 32 + threads - 1) / threads;  // k_warp: one ray per warp at a time
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1), want));
     void* args[] = {(void*)&A, (void*)&n_slots};
-    if (A.fixup_list) XB_CUDA(cudaMemsetAsync(A.fixup_count, 0, sizeof(unsigned long long), s));
     cudaEvent_t* ev = (cudaEvent_t*)A.march_events;
     NvtxRange r_march("march: k_warp");
     if (ev) XB_CUDA(cudaEventRecord(ev[0], s));
