@@ -891,7 +891,7 @@ def bench_ours(args):
 
 def tf_refresh(S):
     """Config 4's interactive TF edit: rebuild the volume active set (per-region
-    majorants, R/accel.py:91-115 + 227-234) for a new ramp; median of 5, warm."""
+    majorants, R/accel.py:91-115 + 227-234) for a new ramp; median of 9 after 3 warm-up rebuilds."""
     import torch
 
     from paper_2009_03076_b200.accel import build_volume_bvh
@@ -902,9 +902,10 @@ def tf_refresh(S):
     from paper_2009_03076_b200 import _native as N
 
     tf2 = [tf_for(S.model.value_range(0), S.cfg, max_alpha=a) for a in (0.3, 0.4)]
-    build_volume_bvh(S.regions, tf2[0], 0, model=S.model)
+    for k in range(3):  # warm: the first rebuilds grow the allocator pools
+        build_volume_bvh(S.regions, tf2[k % 2], 0, model=S.model)
     wall, dev = [], []
-    for k in range(7):
+    for k in range(9):
         gc.collect()
         torch.cuda.synchronize()
         ta = time.perf_counter()
