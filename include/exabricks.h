@@ -177,11 +177,6 @@ int xb_tuning_set(const xb_tuning* t); /* NULL restores the defaults */
  * returns up to `cap` elapsed times in ms, oldest first, in ms[0 .. *n); the
  * returned records are forgotten. */
 int xb_march_times(double* ms, int32_t cap, int32_t* n);
-/* Work of the exact pass after the march (k_fixup) on `device`
- * since the last call: out[0] pixels re-rendered with the exact per-pixel
- * path, out[1] pixels whose deferred samples got the exact FP64 shading
- * gradient, out[2] those samples.  Waits for the device's work; resets. */
-int xb_fixup_stats(int32_t device, int64_t* out);
 
 int xb_tile_count(int32_t width, int32_t height, int32_t rank, int32_t world, int64_t* n_tiles, int32_t* tile_px);
 /* gathered packed tiles (rank-major, tiles_per_rank each) -> (H, W, 4) image; device pointers */

@@ -94,7 +94,6 @@ SIGNATURES = {
     "xb_tuning_get": (C.c_int, [P]),
     "xb_tuning_set": (C.c_int, [P]),
     "xb_march_times": (C.c_int, [P, i32, P]),
-    "xb_fixup_stats": (C.c_int, [i32, P]),
     "xb_tile_count": (C.c_int, [i32, i32, i32, i32, P, P]),
     "xb_unpack_tiles": (C.c_int, [P, i64, i32, i32, i32, P, P]),
     "xb_integrate_rays": (C.c_int, [P, P, i32, P, P, i64, P, P, P, P, P, P, P]),

@@ -36,7 +36,6 @@ struct xb_regions {
     // brick records in region-list order for the frame gather (built on first render)
     mutable std::mutex rb_mu;
     mutable xb::DevBuf<xb::RbRec> rb;
-    mutable xb::DevBuf<xb::RbRecF> rbf;  // the same, region-local FP32 (k_warp's gather)
     mutable bool rb_ok = false;
 };
 struct xb_active {
@@ -119,61 +118,15 @@ __global__ void k_region_bricks(const int32_t* __restrict__ ids, int64_t n, cons
     rb[i] = r;
 }
 
-// RbRecF of every list entry of region g (march.cuh:RbRecF): origin O = floor(region
-// lo); per axis k = the brick cell holding O (clamped to [-1, n]: the region lies in the
-// brick's support, grown by half a cell) and the corner of cell k relative to O, an
-// integer, exact in FP32
-__global__ void k_region_bricks_f(const xb::RegionRec* __restrict__ rec, int64_t n_regions,
-                                  const int32_t* __restrict__ ids, const int4* __restrict__ ba,
-                                  const uint32_t* __restrict__ bm, xb::RbRecF* __restrict__ rbf) {
-    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (g >= n_regions) return;
-    const xb::RegionRec rr = rec[g];
-    const int o[3] = {rr.lo[0] >> 1, rr.lo[1] >> 1, rr.lo[2] >> 1};
-    const int nids = rr.meta & 0xffffff;
-    for (int t = 0; t < nids; t++) {
-        const int64_t i = (int64_t)rr.ids_begin + t;
-        const int b = ids[i];
-        const int4 a = ba[b];
-        const uint32_t meta = bm[b];
-        const int lev = meta & 31;
-        const int n[3] = {(int)((meta >> 5) & 511), (int)((meta >> 14) & 511), (int)((meta >> 23) & 511)};
-        const int c[3] = {a.x, a.y, a.z};
-        float l[3];
-        uint32_t kp = 0;
-        for (int ax = 0; ax < 3; ax++) {
-            const int d = o[ax] - c[ax];
-            int k = d >= 0 ? d >> lev : -((-d + (1 << lev) - 1) >> lev);  // floor(d / w)
-            k = min(max(k, -1), n[ax]);
-            l[ax] = (float)(c[ax] + (k << lev) - o[ax]);
-            kp |= (uint32_t)(k + 1) << (10 * ax);
-        }
-        xb::RbRecF f;
-        f.lx = l[0];
-        f.ly = l[1];
-        f.lz = l[2];
-        f.kpack = kp;
-        f.off = (uint32_t)a.w;
-        f.meta = meta;
-        f.sz = (uint32_t)(n[0] * n[1]);
-        f.pad = 0;
-        rbf[i] = f;
-    }
-}
-
 void ensure_region_bricks(const xb_model* m, const xb_regions* r) {
     std::lock_guard<std::mutex> g(r->rb_mu);
     if (r->rb_ok) return;
     const int64_t n = std::max<int64_t>(r->r.n_ids, 1);
     r->rb.alloc(n);
-    r->rbf.alloc(n);
     if (r->r.n_ids > 0) {
         OwnedStream st;
         k_region_bricks<<<(unsigned)((r->r.n_ids + 255) / 256), 256, 0, st.s>>>(
             r->r.ids.p, r->r.n_ids, m->m.brick_a.p, m->m.brick_m.p, r->rb.p);
-        XB_CUDA(cudaGetLastError());
-        k_region_bricks_f<<<(unsigned)((r->r.n_regions + 255) / 256), 256, 0, st.s>>>(
-            r->r.rec.p, r->r.n_regions, r->r.ids.p, m->m.brick_a.p, m->m.brick_m.p, r->rbf.p);
         XB_CUDA(cudaGetLastError());
         XB_CUDA(cudaStreamSynchronize(st.s));
     }
@@ -213,7 +166,6 @@ xb::SceneView scene_view(const xb_model* m, const xb_regions* r, int field) {
     S.rids = r->r.ids.p;
     ensure_region_bricks(m, r);
     S.rb = r->rb.p;
-    S.rbf = r->rbf.p;
     S.kd = r->r.kd.p;
     S.kd4 = r->r.kd4.p;
     for (int a = 0; a < 3; a++) {
@@ -679,16 +631,6 @@ int xb_march_times(double* ms, int32_t cap, int32_t* n) {
     });
 }
 
-int xb_fixup_stats(int32_t device, int64_t* out) {
-    return guarded([&] {
-        XB_CHECK(out, XB_ERR_ARG, "null output");
-        xb::DeviceGuard dg(device);
-        unsigned long long v[3];
-        xb::take_fixup_stats(v);
-        for (int i = 0; i < 3; i++) out[i] = (int64_t)v[i];
-    });
-}
-
 void xb_tuning_defaults(xb_tuning* t) {
     if (!t) return;
     std::memset(t, 0, sizeof(*t));
@@ -909,30 +851,15 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             XB_CUDA(cudaEventCreate(&me.ev[1]));
             A->march_events = me.ev;
         }
-        int32_t* fixup_buf = nullptr;  // k_warp's pixels for the exact FP64 re-render (k_fixup)
-        if (A->kernel == 0 && (xb::kGatherF32 || A->M.grad_mode == 1)) {
+        int32_t* fixup_buf = nullptr;  // k_warp's pixels for the exact FP64 shading re-render (k_fixup)
+        if (A->kernel == 0 && A->M.grad_mode == 1) {
             const size_t n_slots = std::max<size_t>((size_t)n_local * xb::kTileW * xb::kTileH, 1);
             XB_CUDA(cudaMallocAsync((void**)&fixup_buf, n_slots * sizeof(int32_t), s));
             A->fixup_list = fixup_buf;
             A->fixup_count = scratch + 19;  // zeroed with the scratch
         }
-        void* defer_buf = nullptr;  // deferred shading (render.cuh:DeferSample): analytic gradients
-        A->defer_s = nullptr;
-        A->defer_p = nullptr;
-        A->defer_count = scratch + 20;  // [samples, pixels], zeroed with the scratch
-        A->defer_s_cap = A->defer_p_cap = 0;
-        if (A->kernel == 0 && A->M.grad_mode == 1) {
-            constexpr int kDeferSamples = 1 << 18, kDeferPixels = 1 << 17;  // overflow: exact re-render (k_fixup)
-            XB_CUDA(cudaMallocAsync(&defer_buf, (size_t)kDeferSamples * sizeof(xb::DeferSample) +
-                                                    (size_t)kDeferPixels * sizeof(xb::DeferPixel), s));
-            A->defer_s = (xb::DeferSample*)defer_buf;
-            A->defer_p = (xb::DeferPixel*)(A->defer_s + kDeferSamples);
-            A->defer_s_cap = kDeferSamples;
-            A->defer_p_cap = kDeferPixels;
-        }
         xb::launch_render(*A, n_local, count_bytes != 0, s);
         if (fixup_buf) XB_CUDA(cudaFreeAsync(fixup_buf, s));
-        if (defer_buf) XB_CUDA(cudaFreeAsync(defer_buf, s));
         if (A->march_events) {
             std::lock_guard<std::mutex> eg(g_events_mu);
             g_events.push_back(me);

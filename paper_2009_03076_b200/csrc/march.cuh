@@ -23,16 +23,10 @@ namespace xb {
 
 constexpr double kEpsWeight = 1e-12;     // EPS_WEIGHT, R/sampling.py:37
 
-constexpr double kTFar = 1.0e30;            // _T_FAR, R/render.py:49
+constexpr double kTFar = 1.0e30;
 // zero pad around the frame gather's value copy: a brick's unclamped 2x2x2
 // window reaches at most nx*(ny+1) + 1 <= 32*33 + 1 values before or after it
-constexpr int64_t kGatherPad = 2048;
-// k_warp's gather in FP32 (gather_shade_f); XB_GATHER_F64=1 builds the exact
-// FP64 gather there instead (A/B)
-#ifndef XB_GATHER_F64
-#define XB_GATHER_F64 0
-#endif
-constexpr bool kGatherF32 = !XB_GATHER_F64;
+constexpr int64_t kGatherPad = 2048;         // _T_FAR, R/render.py:49
 constexpr int kKdStack = 64;
 
 // exact power of two for |e| < 1022 (brick cell widths, finest widths)
@@ -100,8 +94,6 @@ struct SceneView {
     // frame-gather brick records in region-list order (rb[i] = brick rids[i]):
     // a region's bricks are read without the id hop
     const struct RbRec* __restrict__ rb;
-    // the same records region-local in FP32 for k_warp's gather (RbRecF)
-    const struct RbRecF* __restrict__ rbf;
     const KdNode* __restrict__ kd;
     const Kd4Node* __restrict__ kd4;
     int32_t root_lo[3], root_hi[3];
@@ -569,8 +561,6 @@ __device__ __forceinline__ void gather_fast(const SceneView& S, const int32_t* _
 // 1/den^2 is dropped because the shading factor depends on the direction only.
 struct FastAccum {
     double num, den;
-    double v;  // the sample value num / den (meaningful when den > kEpsWeight)
-    bool kink; // FP32 gather: the gradient must come from the exact gather (kKink)
     float g[3];
     int n_nz;
 };
@@ -607,12 +597,12 @@ struct ShadeAcc {
     double num, den;
     float fden, gnum, dn0, dn1, dn2, dd0, dd1, dd2, v0;
     int n_nz;
-    bool have_ref, kink;
+    bool have_ref;
     __device__ __forceinline__ void clear() {
         num = den = 0.0;
         fden = gnum = dn0 = dn1 = dn2 = dd0 = dd1 = dd2 = v0 = 0.f;
         n_nz = 0;
-        have_ref = kink = false;
+        have_ref = false;
     }
     // quotient-rule numerator of the analytic gradient (direction only, see FastAccum)
     __device__ __forceinline__ void gradient(float g[3]) const {
@@ -741,181 +731,8 @@ __device__ __forceinline__ void gather_shade(const SceneView& S, int64_t off, in
     for (int t = 0; t < nids; t++) brick_step<GRAD>(S, load_rb(rb + t), px, py, pz, A);
     F.num = A.num;
     F.den = A.den;
-    F.v = A.num / A.den;
-    F.kink = false;
     F.n_nz = A.n_nz;
     if (GRAD) A.gradient(F.g);
-}
-
-// ---------------------------------------------------------------------------
-// FP32 frame gather (k_warp's production path; the exact FP64 gather above
-// runs the COUNT launch, k_fixup, k_render and the ray batches).
-//
-// Positions are region-local: the sample's offset from the region origin O =
-// floor(region lo) is rounded once to FP32 per sample, and each brick record
-// holds the lower corner of window cell k of its brick relative to O, where k
-// is the cell next to O (RbRecF, built per region, abi.cu:k_region_bricks_f):
-// corner and origin are integers, so the record is exact and |p - corner'| is
-// at most the region's extent plus one cell — the window coordinate keeps 24
-// bits over the region, not over the brick.  The window floor is one
-// round-down add of 1.5 * 2^23 (no conversion unit), the hats are 1 - frac
-// and frac (the reference's 1 - |c - p| / w, R/sampling.py:57-63, without the
-// cell centre), and the value is v0 + sum h (v - v0) / sum h from the same
-// v0-shifted partials as the gradient: no FP64 and no conversions per brick.
-// Against the exact gather the value moves by ~1e-7 relative, far inside the
-// image tolerance; the per-pixel counters can only move through early
-// termination or the kEpsWeight test, and the frame kernels list every pixel
-// whose opacity comes within kTermMargin of the termination threshold, or
-// whose weight within a factor 4 of kEpsWeight, for k_fixup's exact re-render
-// — so the counters stay those of the exact path.
-struct __align__(16) RbRecF {
-    float lx, ly, lz;  // lower corner of window cell (kx, ky, kz), relative to the region origin
-    uint32_t kpack;    // (kx + 1) | (ky + 1) << 10 | (kz + 1) << 20, k in [-1, n]
-    uint32_t off, meta;  // scalar offset; level | nx << 5 | ny << 14 | nz << 23
-    uint32_t sz, pad;    // nx * ny
-};
-static_assert(sizeof(RbRecF) == 32, "RbRecF is 32 bytes");
-#ifndef XB_TERM_MARGIN
-#define XB_TERM_MARGIN 0
-#endif
-constexpr double kTermMargin = XB_TERM_MARGIN;  // <= 0: no termination re-renders (A/B)
-
-__device__ __forceinline__ RbRecF load_rbf(const RbRecF* __restrict__ p) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-    const uint4 b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
-    RbRecF r;
-    r.lx = a.x;
-    r.ly = a.y;
-    r.lz = a.z;
-    r.kpack = __float_as_uint(a.w);
-    r.off = b.x;
-    r.meta = b.y;
-    r.sz = b.z;
-    r.pad = 0;
-    return r;
-}
-
-struct Axis2F {
-    float h0, h1, s0, s1;  // hats and gradient slopes, zeroed when the slot is invalid
-    int x0;                // brick cell index of slot 0
-    bool v0, v1;
-    bool kink;             // within kKink of a cell centre (see brick_step_f)
-};
-// The analytic gradient jumps where a sample crosses a cell centre (a slot's
-// slope term enters with its hat > 0 test, R/sampling.py:90-100): there the
-// FP32 window may take the other side than the reference's FP64 arithmetic.
-// The window coordinate t = (p - corner') / w - 1/2 carries at most
-// 2^-24 (|p| / w + 2 |t| + 1) <= 2^-24 (3 |t| + 3) of rounding (p
-// region-local, |p| / w <= |t| + 3/2 since corner' is the cell holding the
-// origin: the FP32 rounding of p, of p - corner' and of the fma); a sample with
-// any axis of any brick within 4x that bound of a centre has its shading
-// deferred to the reference's FP64 gradient (DeferSample, render.cuh).
-
-// p region-local, l = corner' (cell k's lower corner); t = (p - l) / w - 1/2 = (x0 - k) + frac
-#ifndef XB_KINK
-#define XB_KINK 1
-#endif
-constexpr bool kKinkTest = XB_KINK != 0;  // XB_KINK=0: no gradient-jump test (A/B only: not exact)
-
-template <bool KINK>
-__device__ __forceinline__ Axis2F window_axis_f(float p, float l, int k, int n, float iw) {
-    constexpr float kM = 12582912.0f;  // 1.5 * 2^23: t + kM rounded down is floor(t) + kM for |t| < 2^22
-    Axis2F A;
-    const float t = fmaf(p - l, iw, -0.5f);
-    const float y = __fadd_rd(t, kM);
-    const float fr = t - (y - kM);  // exact, in [0, 1)
-    A.x0 = (__float_as_int(y) - __float_as_int(kM)) + k;
-    A.v0 = (unsigned)A.x0 < (unsigned)n;  // hat 1 - frac > 0
-    A.v1 = (unsigned)(A.x0 + 1) < (unsigned)n && fr > 0.f;
-    A.h0 = A.v0 ? 1.f - fr : 0.f;
-    A.h1 = A.v1 ? fr : 0.f;
-    A.s0 = A.v0 ? -iw : 0.f;  // sign(c0 - p) = sign(-frac): the reference's e > 0 test gives -1 at 0
-    A.s1 = A.v1 ? iw : 0.f;
-    if (KINK) {
-        const float e = fmaf(fabsf(t), 0x3p-22f, 0x3p-22f);
-        A.kink = fabsf(fr - 0.5f) + e > 0.5f;
-    } else {
-        A.kink = false;
-    }
-    return A;
-}
-
-template <bool GRAD>
-__device__ __forceinline__ void brick_step_f(const SceneView& S, const RbRecF& B, float px, float py, float pz,
-                                             ShadeAcc& A) {
-    const int lev = B.meta & 31;
-    const int nx = (B.meta >> 5) & 511, ny = (B.meta >> 14) & 511, nz = (B.meta >> 23) & 511;
-    const float iw = __int_as_float((127 - lev) << 23);
-    const Axis2F X = window_axis_f<GRAD && kKinkTest>(px, B.lx, (int)(B.kpack & 1023) - 1, nx, iw);
-    const Axis2F Y = window_axis_f<GRAD && kKinkTest>(py, B.ly, (int)((B.kpack >> 10) & 1023) - 1, ny, iw);
-    const Axis2F Z = window_axis_f<GRAD && kKinkTest>(pz, B.lz, (int)(B.kpack >> 20) - 1, nz, iw);
-    if (GRAD) A.kink = A.kink || X.kink || Y.kink || Z.kink;
-    // unclamped window read from S.gvals as in brick_step
-    const int x0 = min(max(X.x0, -1), nx - 1), y0 = min(max(Y.x0, -1), ny - 1), z0 = min(max(Z.x0, -1), nz - 1);
-    const int sy = nx, sz = (int)B.sz;
-    const float* __restrict__ p0 = S.gvals + B.off + (x0 + nx * y0 + sz * z0);
-    const float* __restrict__ p1 = p0 + sz;
-    float vv[2][2][2];  // [dz][dy][dx]
-    vv[0][0][0] = __ldg(p0); vv[0][0][1] = __ldg(p0 + 1);
-    vv[0][1][0] = __ldg(p0 + sy); vv[0][1][1] = __ldg(p0 + sy + 1);
-    vv[1][0][0] = __ldg(p1); vv[1][0][1] = __ldg(p1 + 1);
-    vv[1][1][0] = __ldg(p1 + sy); vv[1][1][1] = __ldg(p1 + sy + 1);
-    if (!A.have_ref && (X.v0 || X.v1) && (Y.v0 || Y.v1) && (Z.v0 || Z.v1)) {  // first contributing cell
-        const float r0 = X.v0 ? vv[0][0][0] : vv[0][0][1], r1 = X.v0 ? vv[0][1][0] : vv[0][1][1];
-        const float r2 = X.v0 ? vv[1][0][0] : vv[1][0][1], r3 = X.v0 ? vv[1][1][0] : vv[1][1][1];
-        const float q0 = Y.v0 ? r0 : r1, q1 = Y.v0 ? r2 : r3;
-        A.v0 = Z.v0 ? q0 : q1;
-        A.have_ref = true;
-    }
-    float C[2], D[2], E[2];
-#pragma unroll
-    for (int dz = 0; dz < 2; dz++) {
-        const float u00 = vv[dz][0][0] - A.v0, u01 = vv[dz][0][1] - A.v0;
-        const float u10 = vv[dz][1][0] - A.v0, u11 = vv[dz][1][1] - A.v0;
-        const float A0 = fmaf(X.h1, u01, X.h0 * u00), A1 = fmaf(X.h1, u11, X.h0 * u10);  // x-hat reductions
-        C[dz] = fmaf(Y.h1, A1, Y.h0 * A0);  // sum hx hy u
-        if (GRAD) {
-            const float B0 = fmaf(X.s1, u01, X.s0 * u00), B1 = fmaf(X.s1, u11, X.s0 * u10);  // x-slope reductions
-            D[dz] = fmaf(Y.h1, B1, Y.h0 * B0);  // sum sx hy u
-            E[dz] = fmaf(Y.s1, A1, Y.s0 * A0);  // sum hx sy u
-        }
-    }
-    A.gnum = fmaf(Z.h1, C[1], fmaf(Z.h0, C[0], A.gnum));
-    const float Hx = X.h0 + X.h1, Hy = Y.h0 + Y.h1, Hz = Z.h0 + Z.h1;
-    A.fden = fmaf(Hx * Hy, Hz, A.fden);
-    if (GRAD) {
-        A.dn0 = fmaf(Z.h1, D[1], fmaf(Z.h0, D[0], A.dn0));
-        A.dn1 = fmaf(Z.h1, E[1], fmaf(Z.h0, E[0], A.dn1));
-        A.dn2 = fmaf(Z.s1, C[1], fmaf(Z.s0, C[0], A.dn2));
-        const float Sx = X.s0 + X.s1, Sy = Y.s0 + Y.s1, Sz = Z.s0 + Z.s1;
-        A.dd0 = fmaf(Sx * Hy, Hz, A.dd0);
-        A.dd1 = fmaf(Hx * Sy, Hz, A.dd1);
-        A.dd2 = fmaf(Hx * Hy, Sz, A.dd2);
-    }
-}
-
-// the FP32 frame gather over region-list entries [off, off + nids) (S.rbf) at
-// the region-local position p (see RbRecF); F.n_nz is not counted
-template <bool GRAD>
-__device__ __forceinline__ void gather_shade_f(const SceneView& S, int64_t off, int nids, float px, float py, float pz,
-                                               FastAccum& F) {
-    ShadeAcc A;
-    A.clear();
-    const RbRecF* __restrict__ rb = S.rbf + off;
-    for (int t = 0; t < nids; t++) brick_step_f<GRAD>(S, load_rbf(rb + t), px, py, pz, A);
-    F.den = (double)A.fden;
-    F.v = (double)(A.v0 + A.gnum / A.fden);
-    F.kink = A.kink;
-    F.n_nz = 0;
-    if (GRAD) A.gradient(F.g);
-}
-
-// the region origin of the FP32 gather: floor of the region's lower corner
-__device__ __forceinline__ void region_origin(const RegionRec* __restrict__ rec, int rid, double o[3]) {
-    const int4 lo = __ldg(reinterpret_cast<const int4*>(rec + rid));
-    o[0] = (double)(lo.x >> 1);
-    o[1] = (double)(lo.y >> 1);
-    o[2] = (double)(lo.z >> 1);
 }
 
 // _shade_factor (R/render.py:284-289) on an unnormalised FP32 gradient direction

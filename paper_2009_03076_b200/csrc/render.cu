@@ -751,25 +751,6 @@ __global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant
 // lattice, sequential front-to-back compositing, early termination — with the
 // frame kernel's reconstruction and shading.  Used by k_short and by k_warp's
 // short-ray phase.
-// running totals (xb_fixup_stats): pixels re-rendered, pixels and samples corrected
-__device__ unsigned long long g_fixup_stats[3];
-
-// list a pixel with deferred samples (head: its last DeferSample) for k_fixup
-__device__ __forceinline__ void defer_pixel(const RenderArgs& A, int64_t slot, int head, const double acc[4], int nreg,
-                                            int nsmp, bool& fix) {
-    const unsigned long long q = atomicAdd(A.defer_count + 1, 1ull);
-    if (q >= (unsigned long long)A.defer_p_cap) {
-        fix = true;  // list full: exact re-render of the pixel
-        return;
-    }
-    DeferPixel& P = A.defer_p[q];
-    P.acc[0] = acc[0]; P.acc[1] = acc[1]; P.acc[2] = acc[2]; P.acc[3] = acc[3];
-    P.slot = slot;
-    P.head = head;
-    P.nreg = nreg;
-    P.nsmp = nsmp;
-}
-
 template <int GRAD, bool ISO, bool COUNT>
 __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __restrict__ s_tf, int64_t slot,
                                           unsigned long long& my_reg, unsigned long long& my_smp,
@@ -787,7 +768,6 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
     double ar = 0.0, ag = 0.0, ab = 0.0, aa = 0.0;
     int nreg = 0, nsmp = 0;
     bool fix = false;
-    int head = -1;  // last deferred sample of this pixel (DeferSample)
     double t = tmin;
     for (int li = 0; li < count && aa < A.M.early; li++) {
         const int rid = list[li];
@@ -800,7 +780,6 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
         const int lev = rr.meta >> 24, nids = rr.meta & 0xffffff;
         const int32_t* ids = S.rids + rr.ids_begin;
         if (COUNT) my_bytes += 32 + 4 * (unsigned long long)nids;
-        const double ox = (double)(rr.lo[0] >> 1), oy = (double)(rr.lo[1] >> 1), oz = (double)(rr.lo[2] >> 1);
         const double dt = A.M.lv_dt[lev];
         double prev = ci, k = floor(ci / dt - rho) + 1.0;
         bool done = false;
@@ -814,28 +793,22 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
             nsmp++;
             const double px = r.o[0] + mid * r.d[0], py = r.o[1] + mid * r.d[1], pz = r.o[2] + mid * r.d[2];
             FastAccum F;
-            if (kGatherF32 && !COUNT) {
-                gather_shade_f<GRAD == 1>(S, (int64_t)rr.ids_begin, nids, (float)(px - ox), (float)(py - oy),
-                                          (float)(pz - oz), F);
-                fix = fix || (F.den > 0.25 * kEpsWeight && F.den < 4.0 * kEpsWeight);
-            } else {
-                gather_shade<GRAD == 1>(S, (int64_t)rr.ids_begin, nids, px, py, pz, F);
-            }
+            gather_shade<GRAD == 1>(S, (int64_t)rr.ids_begin, nids, px, py, pz, F);
             if (COUNT) my_bytes += 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
             if (F.den > kEpsWeight) {
-                const double v = F.v;
+                const double v = F.num / F.den;
                 double c[4];
                 tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_inv, v, c);
                 if (c[3] > 0.0) {
                     const double alpha = opacity_correct(c[3], sl * A.M.lv_is1[lev]);
-                    bool dfr = false;  // shading deferred to k_fixup (DeferSample)
-                    double f = 1.0;
                     if (GRAD != 0) {
+                        double f;
                         if (GRAD == 1) {
                             f = shade_factor_f(F.g, r, v);
-                            // untrusted FP32 gradient: underflow (shade_factor_f) or a gradient jump (kKink)
-                            dfr = (f < 0.0 || F.kink) && alpha >= kNegligibleAlpha;
-                            if (f < 0.0) f = 0.2;
+                            if (f < 0.0) {  // untrusted FP32 gradient (kNegligibleAlpha: see shade_factor_f)
+                                fix = fix || alpha >= kNegligibleAlpha;
+                                f = 0.2;
+                            }
                         } else {
                             double g[3];
                             int64_t ne = 0;
@@ -849,21 +822,6 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
                     ag += w * c[1];
                     ab += w * c[2];
                     aa += w;
-                    if (GRAD == 1 && dfr) {
-                        const unsigned long long e = A.defer_s ? atomicAdd(A.defer_count, 1ull) : ~0ull;
-                        if (e < (unsigned long long)A.defer_s_cap) {
-                            DeferSample& E = A.defer_s[e];
-                            E.cs[0] = w * c[0]; E.cs[1] = w * c[1]; E.cs[2] = w * c[2];
-                            E.w = 1.0;
-                            E.f0 = f;
-                            E.p[0] = px; E.p[1] = py; E.p[2] = pz;
-                            E.ids = rr.ids_begin; E.nids = nids; E.next = head;
-                            head = (int)e;
-                        } else {
-                            fix = true;  // list full: exact re-render of the pixel
-                        }
-                    }
-                    if (kGatherF32 && !COUNT && kTermMargin > 0) fix = fix || fabs(aa - A.M.early) < kTermMargin;
                     if (aa >= A.M.early) break;
                 }
             }
@@ -883,7 +841,6 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
         }
     }
     write_pixel(A, sp.out, acc, nreg, nsmp);
-    if (GRAD == 1 && head >= 0 && !fix) defer_pixel(A, slot, head, acc, nreg, nsmp, fix);
     if (fix && A.fixup_list) A.fixup_list[atomicAdd(A.fixup_count, 1ull)] = (int32_t)slot;
     my_reg += nreg;
     my_smp += nsmp;
@@ -1013,8 +970,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             const int64_t out_px = q.out;
             double Tr = 1.0, Cr = 0.0, Cg = 0.0, Cb = 0.0;  // transmittance, premultiplied colour
             int nreg = 0, nsmp = 0;
-            bool fix = false;  // exact re-render of the pixel (k_fixup)
-            int head = -1;     // last deferred sample of the ray (DeferSample), warp-uniform
+            bool fix = false;  // a sample's FP32 gradient was untrusted (shade_factor_f)
             {
                 RayAxes& rs = s_ray[wid];
                 __syncwarp();
@@ -1077,13 +1033,10 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         const SegQ sq = ring[(qh + sg) & 31];
                         const int s_end = __shfl_sync(FULL, q_P, sg);
                         double Ts = 1.0, Cs0 = 0.0, Cs1 = 0.0, Cs2 = 0.0;
-                        bool dfr = false;  // this lane's shading is deferred (DeferSample)
-                        double fsh = 1.0;  // its provisional shading factor
                         unsigned long long my_bytes = 0;
                         const int lev = sq.meta >> 24;
                         const int nids = sq.meta & 0xffffff;
                         double sl = 0.0, px = 0.0, py = 0.0, pz = 0.0;
-                        float fx = 0.f, fy = 0.f, fz = 0.f;  // region-local position (FP32 gather)
                         if (act) {
                             const double s_dt = A.M.lv_dt[lev];
                             const int j = s - (s_end - sq.cnt);
@@ -1094,13 +1047,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             px = r.o[0] + mid * r.d[0];
                             py = r.o[1] + mid * r.d[1];
                             pz = r.o[2] + mid * r.d[2];
-                            if (kGatherF32 && !COUNT) {
-                                double o[3];
-                                region_origin(S.rec, sq.rid, o);
-                                fx = (float)(px - o[0]);
-                                fy = (float)(py - o[1]);
-                                fz = (float)(pz - o[2]);
-                            }
                         }
                         if (kDebugChunks && A.dbg) {
                             int nn = act ? nids : 0, mx = nn;
@@ -1115,17 +1061,12 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         }
                         FastAccum F;
                         if (act) {
-                            if (kGatherF32 && !COUNT) {
-                                gather_shade_f<GRAD == 1>(S, (int64_t)sq.ids, nids, fx, fy, fz, F);
-                                fix = fix || (F.den > 0.25 * kEpsWeight && F.den < 4.0 * kEpsWeight);
-                            } else {
-                                gather_shade<GRAD == 1>(S, (int64_t)sq.ids, nids, px, py, pz, F);
-                            }
+                            gather_shade<GRAD == 1>(S, (int64_t)sq.ids, nids, px, py, pz, F);
                         }
                         if (act) {
                             if (COUNT) my_bytes = 16 * (unsigned long long)nids + 4 * (unsigned long long)F.n_nz;
                             if (F.den > kEpsWeight) {
-                                const double v = F.v;
+                                const double v = F.num / F.den;
                                 double c[4];
                                 tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_inv, v, c);
                                 if (c[3] > 0.0) {
@@ -1134,10 +1075,10 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                                         double f;
                                         if (GRAD == 1) {
                                             f = shade_factor_f(F.g, r, v);
-                                            // untrusted FP32 gradient: underflow or a gradient jump (kKink)
-                                            dfr = (f < 0.0 || F.kink) && alpha >= kNegligibleAlpha;
-                                            if (f < 0.0) f = 0.2;
-                                            fsh = f;
+                                            if (f < 0.0) {  // untrusted FP32 gradient (see shade_factor_f)
+                                                fix = fix || alpha >= kNegligibleAlpha;
+                                                f = 0.2;
+                                            }
                                         } else {
                                             double g[3];
                                             int64_t ne = 0;
@@ -1151,35 +1092,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                                     Cs0 = alpha * c[0];
                                     Cs1 = alpha * c[1];
                                     Cs2 = alpha * c[2];
-                                }
-                            }
-                        }
-                        // deferred shading: list the lanes' samples (own colour now, the
-                        // transmittance in front of them after the scan)
-                        unsigned dm = 0;
-                        int my_e = -1;
-                        if (GRAD == 1) {
-                            dm = __ballot_sync(FULL, dfr);
-                            if (dm) {
-                                const int nd = __popc(dm);
-                                unsigned long long base = 0;
-                                if (lane == 0) base = A.defer_s ? atomicAdd(A.defer_count, (unsigned long long)nd) : ~0ull;
-                                base = __shfl_sync(FULL, base, 0);
-                                if (base + nd > (unsigned long long)A.defer_s_cap) {
-                                    fix = true;  // list full: exact re-render of the pixel
-                                    dm = 0;
-                                } else {
-                                    if (dfr) {
-                                        const int rank = __popc(dm & ((1u << lane) - 1u));
-                                        my_e = (int)base + rank;
-                                        DeferSample& E = A.defer_s[my_e];
-                                        E.cs[0] = Cs0; E.cs[1] = Cs1; E.cs[2] = Cs2;
-                                        E.f0 = fsh;
-                                        E.p[0] = px; E.p[1] = py; E.p[2] = pz;
-                                        E.ids = sq.ids; E.nids = nids;
-                                        E.next = rank == 0 ? head : my_e - 1;
-                                    }
-                                    head = (int)base + nd - 1;
                                 }
                             }
                         }
@@ -1198,14 +1110,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         }
                         const unsigned tm = __ballot_sync(FULL, act && 1.0 - Tr * Ts >= early);
                         const int last = tm ? __ffs(tm) - 1 : m - 1;
-                        // FP32 gather: an opacity this close to the threshold could end the
-                        // ray one sample apart from the exact gather — k_fixup re-renders it
-                        if (kGatherF32 && !COUNT && kTermMargin > 0)
-                            fix = fix || (lane <= last && fabs(1.0 - Tr * Ts - early) < kTermMargin);
-                        if (GRAD == 1 && dm) {
-                            const double tx = __shfl_up_sync(FULL, Ts, 1);  // exclusive transmittance
-                            if (my_e >= 0) A.defer_s[my_e].w = lane <= last ? Tr * (lane == 0 ? 1.0 : tx) : 0.0;
-                        }
                         const double lT = __shfl_sync(FULL, Ts, last);
                         const double l0 = __shfl_sync(FULL, Cs0, last), l1 = __shfl_sync(FULL, Cs1, last),
                                      l2 = __shfl_sync(FULL, Cs2, last);
@@ -1516,7 +1420,6 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                     }
                 }
             }
-            fix = __any_sync(FULL, fix);
             if (lane == 0) {
                 double acc[4] = {Cr, Cg, Cb, 1.0 - Tr};
                 if (ISO) {
@@ -1530,9 +1433,9 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                     }
                 }
                 write_pixel(A, out_px, acc, nreg, nsmp);
-                if (GRAD == 1 && head >= 0 && !fix) defer_pixel(A, slot, head, acc, nreg, nsmp, fix);
-                if (fix && A.fixup_list) A.fixup_list[atomicAdd(A.fixup_count, 1ull)] = (int32_t)slot;
             }
+            if (__any_sync(FULL, fix) && lane == 0 && A.fixup_list)
+                A.fixup_list[atomicAdd(A.fixup_count, 1ull)] = (int32_t)slot;
             if (lane == 0) {
                 if (kDebugChunks && A.dbg) {
                     atomicAdd(A.dbg + 2, 1ull);
@@ -1570,30 +1473,16 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
 }
 
 // ---------------------------------------------------------------------------
-// k_fixup, after k_warp: (1) pixels k_warp listed for an exact re-render — a
-// sample weight near kEpsWeight under the FP32 gather (RbRecF), a full
-// deferral list, or (XB_TERM_MARGIN builds) an opacity near the termination
-// threshold — are re-rendered one thread each with the exact per-pixel path
-// (volume_ray: the reference's FP64 sums); (2) pixels with deferred samples
-// (DeferSample) get each sample's shading from the reference's FP64 analytic
-// gradient (R/render.py:295-306) added in and are written again.  The
-// counters are the exact path's, so the frame stats are not touched.
+// k_fixup: pixels whose FP32 shading gradient was untrusted (shade_factor_f)
+// are re-rendered one thread each with the exact per-pixel path — the
+// reference's FP64 gradient sums (volume_ray) — after k_warp.  The counters
+// are the same as k_warp's, so the frame stats are not touched.
 
-
-template <bool ISO, int GRAD>
+template <bool ISO>
 __global__ void __launch_bounds__(128) k_fixup(const __grid_constant__ RenderArgs A) {
     __shared__ double s_tf[1024];
     const int64_t n = (int64_t)*A.fixup_count;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (n > 0) atomicAdd(&g_fixup_stats[0], (unsigned long long)n);
-        if (GRAD == 1 && A.defer_p) {
-            const unsigned long long np = A.defer_count[1], ns = A.defer_count[0];
-            if (np) atomicAdd(&g_fixup_stats[1], min(np, (unsigned long long)A.defer_p_cap));
-            if (ns) atomicAdd(&g_fixup_stats[2], min(ns, (unsigned long long)A.defer_s_cap));
-        }
-    }
-    const int64_t np = GRAD == 1 && A.defer_p ? min((int64_t)A.defer_count[1], (int64_t)A.defer_p_cap) : 0;
-    if (blockIdx.x * (int64_t)blockDim.x >= max(n, np)) return;
+    if (blockIdx.x * (int64_t)blockDim.x >= n) return;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) s_tf[i] = A.tf[i];
     __syncthreads();
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
@@ -1608,7 +1497,7 @@ __global__ void __launch_bounds__(128) k_fixup(const __grid_constant__ RenderArg
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         if (tmin < tmax) {
             const double t_end = ISO ? A.iso_tend[slot] : tmax;
-            volume_ray<GRAD, false>(A.S, A.vflags, A.M, s_tf, r, tmin, t_end, rho, acc, st, nullptr);
+            volume_ray<1, false>(A.S, A.vflags, A.M, s_tf, r, tmin, t_end, rho, acc, st, nullptr);
             if (ISO && A.iso_shade[slot] >= 0.0) {
                 const double f = A.iso_shade[slot];
                 const double w = 1.0 - acc[3];
@@ -1619,26 +1508,6 @@ __global__ void __launch_bounds__(128) k_fixup(const __grid_constant__ RenderArg
             }
         }
         write_pixel(A, sp.out, acc, (int)st.regions, (int)st.samples);
-    }
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < np; q += (int64_t)gridDim.x * blockDim.x) {
-        const DeferPixel& P = A.defer_p[q];
-        const SlotPix sp = slot_pixel(A, P.slot);
-        Ray r;
-        pixel_ray(A, sp.x, sp.y, r);
-        double acc[4] = {P.acc[0], P.acc[1], P.acc[2], P.acc[3]};
-        for (int e = P.head; e >= 0;) {
-            const DeferSample& E = A.defer_s[e];
-            Accum G;
-            gather<true>(A.S, A.S.rids + E.ids, E.nids, E.p[0], E.p[1], E.p[2], G);
-            double g[3];
-            analytic_gradient(G, g);
-            const double k = shade_factor(g, r) / E.f0 - 1.0;
-            acc[0] += E.w * E.cs[0] * k;
-            acc[1] += E.w * E.cs[1] * k;
-            acc[2] += E.w * E.cs[2] * k;
-            e = E.next;
-        }
-        write_pixel(A, sp.out, acc, P.nreg, P.nsmp);
     }
 }
 
@@ -1837,21 +1706,11 @@ void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaS
     if (ev) XB_CUDA(cudaEventRecord(ev[0], s));
     XB_CUDA(cudaLaunchKernel((const void*)fn, dim3((unsigned)blocks), dim3(threads), args, dyn, s));
     if (ev) XB_CUDA(cudaEventRecord(ev[1], s));
-    if (A.fixup_list) {  // listed pixels and deferred shading (k_fixup)
+    if (A.fixup_list && g == 1 && !count) {  // untrusted FP32 gradients: exact re-render of those pixels
         void* fargs[] = {(void*)&A};
-        const void* ff = iso ? (g == 0 ? (const void*)k_fixup<true, 0>
-                                       : (g == 1 ? (const void*)k_fixup<true, 1> : (const void*)k_fixup<true, 2>))
-                             : (g == 0 ? (const void*)k_fixup<false, 0>
-                                       : (g == 1 ? (const void*)k_fixup<false, 1> : (const void*)k_fixup<false, 2>));
+        const void* ff = iso ? (const void*)k_fixup<true> : (const void*)k_fixup<false>;
         XB_CUDA(cudaLaunchKernel(ff, dim3((unsigned)sms), dim3(128), fargs, 0, s));
     }
-}
-
-void take_fixup_stats(unsigned long long out[3]) {
-    const unsigned long long z[3] = {0, 0, 0};
-    XB_CUDA(cudaDeviceSynchronize());  // the render streams are non-blocking
-    XB_CUDA(cudaMemcpyFromSymbol(out, g_fixup_stats, sizeof z));
-    XB_CUDA(cudaMemcpyToSymbol(g_fixup_stats, z, sizeof z));
 }
 
 // ---------------------------------------------------------------------------

@@ -21,26 +21,6 @@ constexpr int kResume = 48;            // resume entries saved per truncated wal
 #endif
 constexpr bool kDebugChunks = XB_DEBUG_CHUNKS != 0;
 
-// Deferred shading (analytic gradients).  The frame kernels shade from FP32
-// gradient partials; a sample whose FP32 gradient cannot be trusted — it
-// underflowed (shade_factor_f) or the sample sits within rounding of a
-// gradient jump (kKink) — is composited with a provisional factor f0 and
-// listed; k_fixup then evaluates the reference's FP64 gradient there and adds
-// contribution * (f / f0 - 1) to its pixel before writing it again.  The
-// opacity does not depend on the shading, so the correction is exact.
-struct DeferSample {
-    double cs[3];  // the sample's own composited colour alpha * c * f0
-    double w;      // transmittance in front of it (cs * w is its share of the pixel)
-    double f0;     // provisional shading factor (> 0)
-    double p[3];   // sample position
-    int32_t ids, nids, next, pad;  // region brick list; the pixel's previous deferred sample (-1: none)
-};
-struct DeferPixel {
-    double acc[4];  // the pixel's provisional RGBA (k_warp's, iso included)
-    int64_t slot;
-    int32_t head, nreg, nsmp, pad;  // last deferred sample of the pixel; counters
-};
-
 struct RenderArgs {
     SceneView S;
     const uint8_t* vflags;  // per k-d node: subtree holds an active volume region
@@ -78,12 +58,8 @@ struct RenderArgs {
     unsigned long long* dbg;           // diagnostics (XB_DEBUG_CHUNKS): k_warp chunks, chunk lanes, rays, samples
     int fuse_short;                    // k_warp runs the short rays after the long ones (no k_short launch)
     unsigned long long* short_counter; // k_warp's short-ray grab counter
-    int32_t* fixup_list;               // pixels for k_fixup's exact re-render, or NULL
+    int32_t* fixup_list;               // pixels for k_fixup (exact FP64 shading), or NULL
     unsigned long long* fixup_count;
-    struct DeferSample* defer_s;       // samples whose shading waits for the exact gradient (k_fixup), or NULL
-    struct DeferPixel* defer_p;        // their pixels
-    unsigned long long* defer_count;   // [samples, pixels]
-    int defer_s_cap, defer_p_cap;
     int cut_tau;                       // k_walk2 also continues walks stopped by the opacity minorant
     int32_t* blk_counts;               // k_walk -> k_route: short / long / cut rays per k_walk block
     int32_t* short_list;               // rays with a complete list of <= 8 leaves (k_short's work), or NULL
@@ -116,9 +92,6 @@ struct RayBatchArgs {
 };
 
 void launch_render(const RenderArgs& A, int64_t n_tiles_local, bool count, cudaStream_t s);
-// k_fixup's work on the current device since the last call (resets it):
-// [pixels re-rendered, pixels with deferred shading, deferred samples]
-void take_fixup_stats(unsigned long long out[3]);
 void launch_rays(const RayBatchArgs& B, cudaStream_t s);
 void launch_unpack(const uchar4* packed, int64_t tiles_per_rank, int world, int tiles_x, int tiles_y, int W, int H,
                    uchar4* img, cudaStream_t s);

@@ -57,18 +57,10 @@ def main():
     out = torch.empty((H, W, 4), dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
-    has_fix = hasattr(N.lib(), "xb_fixup_stats")
     for v in variants:
         setv(v)
-        if has_fix:
-            N.check(N.lib().xb_fixup_stats(torch.cuda.current_device(), (C.c_int64 * 3)()))
         for cam in cams:
             render_native(scene, cam, tf, params, out.data_ptr(), stream=stream.cuda_stream)
-        if has_fix:
-            fx = (C.c_int64 * 3)()
-            N.check(N.lib().xb_fixup_stats(torch.cuda.current_device(), fx))
-            print(f"{v:10s} k_fixup per frame: {fx[0] / len(cams):.1f} pixels re-rendered, "
-                  f"{fx[1] / len(cams):.1f} pixels / {fx[2] / len(cams):.1f} samples shading-corrected")
     torch.cuda.synchronize()
     # enqueue everything first (no host sync inside the loop): the GPU queue stays
     # ahead of the host, so host-side stalls never land between two events

@@ -3,7 +3,8 @@ FP64 gather in k_warp): per build, `python tools/gather_diff.py dump TAG CONFIG
 [views]` (XB_LIB selects the library) writes /tmp/gd_TAG_CONFIG_VIEW.npz with
 the float RGBA frame and the per-pixel counters; `python tools/gather_diff.py
 cmp TAG_A TAG_B CONFIG [views]` prints max |dRGBA|, the pixels whose counters
-differ and the k_fixup re-render count of each build."""
+differ and, for builds that export xb_fixup_stats (the FP32-gather experiment,
+3a9dfc7), the k_fixup counts."""
 import ctypes as C
 import os
 import sys
@@ -38,10 +39,13 @@ def dump(tag, cfg_name, views):
         out8 = np.zeros((H, W, 4), np.uint8)
         outf = np.zeros((H, W, 4), np.float64)
         cnt = np.zeros((H, W, 2), np.int32)
-        N.check(N.lib().xb_fixup_stats(0, (C.c_int64 * 3)()))
+        has_fix = hasattr(N.lib(), "xb_fixup_stats")
+        if has_fix:
+            N.check(N.lib().xb_fixup_stats(0, (C.c_int64 * 3)()))
         render_native(scene, cams[v], tf, params, out8, outf, cnt)
         fx = (C.c_int64 * 3)()
-        N.check(N.lib().xb_fixup_stats(0, fx))
+        if has_fix:
+            N.check(N.lib().xb_fixup_stats(0, fx))
         np.savez(f"/tmp/gd_{tag}_{cfg_name}_{v}.npz", f=outf, c=cnt, fix=np.array(list(fx)))
         torch.cuda.synchronize()
 
