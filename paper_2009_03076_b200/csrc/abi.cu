@@ -768,8 +768,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         // per-call scratch (stream-ordered pool): [regions, samples, bytes, work counter, list lengths x5,
         // debug counters x7, short-ray grab counter]
         unsigned long long* scratch = nullptr;
-        XB_CUDA(cudaMallocAsync((void**)&scratch, 24 * sizeof(unsigned long long), s));
-        XB_CUDA(cudaMemsetAsync(scratch, 0, 24 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMallocAsync((void**)&scratch, 32 * sizeof(unsigned long long), s));
+        XB_CUDA(cudaMemsetAsync(scratch, 0, 32 * sizeof(unsigned long long), s));
         A->walk_counter = scratch + 4;
         unsigned long long* dstats = (stats || count_bytes) ? scratch : nullptr;
         A->stats = dstats;
@@ -865,13 +865,15 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
             g_events.push_back(me);
         }
         if (A->dbg) {
-            unsigned long long d[7];
+            unsigned long long d[20];
             XB_CUDA(cudaMemcpyAsync(d, A->dbg, sizeof d, cudaMemcpyDeviceToHost, s));
             XB_CUDA(cudaStreamSynchronize(s));
             fprintf(stderr, "xb_render: k_warp %llu rays, %llu samples, %llu regions, %llu chunks, %.1f lanes/chunk, "
                             "%.2f bricks/sample, %.2f max bricks/chunk\n",
                     d[2], d[3], d[4], d[0], d[0] ? (double)d[1] / (double)d[0] : 0.0,
                     d[1] ? (double)d[5] / (double)d[1] : 0.0, d[0] ? (double)d[6] / (double)d[0] : 0.0);
+            fprintf(stderr, "xb_render: k_warp warp-cycles: long phase %.3g (rays %.3g, chunks %.3g), short phase %.3g\n",
+                    (double)d[19], (double)d[17], (double)d[16], (double)d[18]);
         }
         if (leaf_buf) XB_CUDA(cudaFreeAsync(leaf_buf, s));
         if (iso_buf) XB_CUDA(cudaFreeAsync(iso_buf, s));

@@ -888,6 +888,8 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     const SceneView& S = A.S;
     const double early = A.M.early;
     unsigned long long tot_reg = 0, tot_smp = 0, tot_bytes = 0;
+    long long cyc_chunk = 0, cyc_ray = 0, cyc_short = 0;  // DEBUG_CHUNKS: per-warp clock64 sums
+    const long long k_t0 = kDebugChunks ? clock64() : 0;
     // work: the long list, or long + short merged when the short rays are too few for k_short
     const bool merged = A.leaves && (!A.short_list || (int64_t)A.walk_counter[0] < A.short_min);
     const int32_t* __restrict__ work = merged ? A.any_list : A.long_list;
@@ -958,6 +960,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             const int src = __ffs(todo) - 1;
             todo &= todo - 1;
             const RaySetup& q = s_setup[wid][src];
+            const long long r_t0 = kDebugChunks ? clock64() : 0;
             Ray r;
 #pragma unroll
             for (int a = 0; a < 3; a++) {
@@ -1016,6 +1019,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                     const int pending = tailP - h0;
                     if (pending >= 32 || (!walk && pending > 0)) {
                         // ================= one chunk of (up to) 32 samples
+                        const long long c_t0 = kDebugChunks ? clock64() : 0;
                         const int m = min(32, pending);
                         if (kDebugChunks && A.dbg && lane == 0) {
                             atomicAdd(A.dbg, 1ull);
@@ -1124,6 +1128,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             nreg += sg_last + 1;
                             if (COUNT && lane <= sg_last)
                                 tot_bytes += 32 + 4 * (unsigned long long)(ring[(qh + lane) & 31].meta & 0xffffff);
+                            if (kDebugChunks) cyc_chunk += clock64() - c_t0;
                             break;
                         }
                         nsmp += m;
@@ -1142,6 +1147,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             tailP -= done;
                             nreg += k;
                         }
+                        if (kDebugChunks) cyc_chunk += clock64() - c_t0;
                         continue;
                     }
                     if (!walk) break;
@@ -1436,6 +1442,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             }
             if (__any_sync(FULL, fix) && lane == 0 && A.fixup_list)
                 A.fixup_list[atomicAdd(A.fixup_count, 1ull)] = (int32_t)slot;
+            if (kDebugChunks) cyc_ray += clock64() - r_t0;
             if (lane == 0) {
                 if (kDebugChunks && A.dbg) {
                     atomicAdd(A.dbg + 2, 1ull);
@@ -1449,6 +1456,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
     }
     // ---- short-ray phase (k_short fused): one short ray per lane, 32 per grab;
     //      cheap, uniform rays fill the tail of the long-ray phase
+    const long long s_t0 = kDebugChunks ? clock64() : 0;
     if (A.fuse_short && A.leaves && !merged) {
         const int64_t n_sh = (int64_t)A.walk_counter[0];
         for (;;) {
@@ -1459,6 +1467,13 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
             const int64_t i = (int64_t)c0 + lane;
             if (i < n_sh) short_ray<GRAD, ISO, COUNT>(A, s_tf, (int64_t)A.short_list[i], tot_reg, tot_smp, tot_bytes);
         }
+    }
+    if (kDebugChunks && A.dbg && lane == 0) {
+        cyc_short = clock64() - s_t0;
+        atomicAdd(A.dbg + 16, (unsigned long long)cyc_chunk);
+        atomicAdd(A.dbg + 17, (unsigned long long)cyc_ray);
+        atomicAdd(A.dbg + 18, (unsigned long long)cyc_short);
+        atomicAdd(A.dbg + 19, (unsigned long long)(s_t0 - k_t0));
     }
     for (int o = 16; o > 0; o >>= 1) {
         tot_reg += __shfl_xor_sync(FULL, tot_reg, o);
