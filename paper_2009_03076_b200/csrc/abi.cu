@@ -203,6 +203,8 @@ void fill_march(xb::MarchConst& M, const xb_march* mp) {
         M.lv_dt[l] = fw / (M.spc * M.rate);
         M.lv_s1[l] = fw / M.spc;
         M.lv_is1[l] = 1.0 / M.lv_s1[l];
+        int ex = 0;
+        M.lv_idt[l] = std::frexp(M.lv_dt[l], &ex) == 0.5 ? std::ldexp(1.0, 1 - ex) : 0.0;  // dt = 2^(ex-1)
     }
 }
 

@@ -929,9 +929,18 @@ struct MarchConst {
     // host-computed per finest level (IEEE division on the host, same values
     // as the kernel would compute): dt = fw/(spc*rate), s1 = fw/spc (R/render.py:402-403)
     double lv_dt[32], lv_s1[32], lv_is1[32];
+    // 1/dt when dt is a power of two (x / dt == x * (1/dt) exactly), else 0 (divide)
+    double lv_idt[32];
     double tf_inv;  // 1/(tf_hi - tf_lo)
     int use_tree;   // cell-location gather through the split tree (render_frame(use_celllocation=True))
 };
+
+// x / dt of the lattice (R/render.py:404-418) for level `lev`: one multiply
+// when dt is a power of two (the bench configs), an IEEE division otherwise
+__device__ __forceinline__ double div_dt(const MarchConst& M, int lev, double x) {
+    const double idt = M.lv_idt[lev];
+    return idt != 0.0 ? x * idt : x / M.lv_dt[lev];
+}
 
 struct RayStats {
     int64_t regions, samples, bytes;

@@ -211,15 +211,17 @@ __device__ __forceinline__ int kd4_child(const Kd4Node& nd, int s) {
 
 // lattice of one region visit (R/render.py:404-418): the samples are the k in
 // [kf, ke) with t_in < dt*(k+rho) < t_out, plus the final one at t_out.
-__device__ __forceinline__ void lattice(double ci, double co, double dt, double rho, double& kf, int& cnt) {
-    double k = floor(ci / dt - rho) + 1.0;
+__device__ __forceinline__ void lattice(const MarchConst& M, int lev, double ci, double co, double rho, double& kf,
+                                        int& cnt) {
+    const double dt = M.lv_dt[lev];
+    double k = floor(div_dt(M, lev, ci) - rho) + 1.0;
     for (;;) {  // skipped lattice points (tk <= t_in): at most a couple
         const double tk = dt * (k + rho);
         if (tk >= co || tk > ci) break;
         k += 1.0;
     }
     kf = k;
-    double ke = floor(co / dt - rho);
+    double ke = floor(div_dt(M, lev, co) - rho);
     if (ke < kf) ke = kf;
     while (ke > kf && dt * ((ke - 1.0) + rho) >= co) ke -= 1.0;
     while (dt * (ke + rho) < co) ke += 1.0;
@@ -666,7 +668,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_iso_warp(const __grid_constant
             const double dt = A.M.lv_dt[rr.meta >> 24];
             double kf;
             int cnt;
-            lattice(ci, co, dt, rho, kf, cnt);  // points p_0 = t_in, p_1..p_cnt (p_cnt = t_out)
+            lattice(A.M, rr.meta >> 24, ci, co, rho, kf, cnt);  // points p_0 = t_in, p_1..p_cnt (p_cnt = t_out)
             double carry_f = 0.0, carry_t = ci;
             bool carry_ok = false, hit = false;
             double th = 0.0, g[3] = {0.0, 0.0, 0.0};
@@ -781,7 +783,7 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
         const int32_t* ids = S.rids + rr.ids_begin;
         if (COUNT) my_bytes += 32 + 4 * (unsigned long long)nids;
         const double dt = A.M.lv_dt[lev];
-        double prev = ci, k = floor(ci / dt - rho) + 1.0;
+        double prev = ci, k = floor(div_dt(A.M, lev, ci) - rho) + 1.0;
         bool done = false;
         while (!done) {
             double tk = dt * (k + rho);
@@ -1398,7 +1400,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                         }
                         double g_kf = 0.0;
                         int g_cnt = 0;
-                        if (lane < ns) lattice(g_ci, g_co, A.M.lv_dt[g_meta >> 24], rho, g_kf, g_cnt);
+                        if (lane < ns) lattice(A.M, g_meta >> 24, g_ci, g_co, rho, g_kf, g_cnt);
                         int P = g_cnt;
 #pragma unroll
                         for (int o = 1; o < 32; o <<= 1) {
