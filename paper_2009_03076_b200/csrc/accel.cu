@@ -135,15 +135,15 @@ void build_active(const DevRegions& R, int kind, int field, double tf_lo, double
     out.device = R.device;
     out.kind = kind;
     const int64_t n = R.n_regions;
-    out.act.alloc(n + 1);
-    out.flags.alloc(R.n_kd + 1);
+    out.act.alloc_async(n + 1, s);
+    out.flags.alloc_async(R.n_kd + 1, s);
     const int BS = 256;
     if (n > 0) {
         if (kind == 0) {
             AlphaTab tab;
             for (int i = 0; i < 256; i++) tab.a[i] = rgba_host[4 * i + 3];
             k_volume_active<<<grid_for(n, BS), BS, 0, s>>>(n, R.n_fields, field, R.vrange.p, tf_lo, tf_hi, tab, out.act.p);
-            out.qmin.alloc(n);
+            out.qmin.alloc_async(n, s);
             k_volume_minorant<<<grid_for(n, BS), BS, 0, s>>>(n, R.n_fields, field, R.vrange.p, tf_lo, tf_hi, tab,
                                                               R.rec.p, out.qmin.p);
         } else if (kind == 1) {
@@ -160,17 +160,18 @@ void build_active(const DevRegions& R, int kind, int field, double tf_lo, double
     }
     check_launch("k_flags_level");
     build_kd4_mask(R, out.flags.p, out.mask4, s);
-    // active id list (ascending) for RegionBvh.prims / n_active
-    CubTemp tmp;
-    DevBuf<int32_t> a32(n + 1), pos(n + 1);
+    // active id list (ascending) for RegionBvh.prims / n_active; scratch from
+    // the stream's pool and prims sized for every region, so the only host
+    // synchronisation is the final count read
+    CubPoolTemp tmp(s);
+    PoolBuf<int32_t> a32(n + 1, s), pos(n + 1, s);
     if (n > 0) k_u8_to_i32<<<grid_for(n, BS), BS, 0, s>>>(n, out.act.p, a32.p);
     XB_CUDA(cudaMemsetAsync(a32.p + n, 0, 4, s));
     exclusive_sum(tmp, a32.p, pos.p, n + 1, s);
-    out.n_active = read_scalar(pos.p + n, s);
-    out.prims.alloc(out.n_active + 1);
+    out.prims.alloc_async(n + 1, s);
     if (n > 0) k_compact_active<<<grid_for(n, BS), BS, 0, s>>>(n, out.act.p, pos.p, out.prims.p);
     check_launch("k_compact_active");
-    XB_CUDA(cudaStreamSynchronize(s));
+    out.n_active = read_scalar(pos.p + n, s);
 }
 
 // ---------------------------------------------------------------------------

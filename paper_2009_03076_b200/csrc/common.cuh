@@ -74,6 +74,14 @@ struct DevBuf {
         n = count;
         if (count) XB_CUDA(cudaMalloc(&p, count * sizeof(T)));
     }
+    // from the device's memory pool, ordered on stream s (no implicit device
+    // synchronisation, retained pool memory: the TF-edit path); release() is
+    // cudaFree, which accepts pool memory and waits for every stream using it
+    void alloc_async(size_t count, cudaStream_t s) {
+        release();
+        n = count;
+        if (count) XB_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), s));
+    }
     void ensure(size_t count) {  // grow-only
         if (count > n) alloc(count + count / 4 + 64);
     }
@@ -94,6 +102,24 @@ struct DevBuf {
         download(v.data(), count, s);
         XB_CUDA(cudaStreamSynchronize(s));
         return v;
+    }
+};
+
+// stream-ordered scratch from the device's memory pool (cudaMallocAsync):
+// no implicit device synchronisation on allocation or release, unlike
+// cudaMalloc / cudaFree — a TF edit or a build never waits for other streams'
+// renders
+template <class T>
+struct PoolBuf {
+    T* p = nullptr;
+    cudaStream_t s;
+    PoolBuf(size_t count, cudaStream_t st) : s(st) {
+        if (count) XB_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), s));
+    }
+    PoolBuf(const PoolBuf&) = delete;
+    PoolBuf& operator=(const PoolBuf&) = delete;
+    ~PoolBuf() {
+        if (p) cudaFreeAsync(p, s);
     }
 };
 

@@ -103,7 +103,7 @@ void build_kd4(DevRegions& R, cudaStream_t s) {
 }
 
 void build_kd4_mask(const DevRegions& R, const uint8_t* flags, DevBuf<uint8_t>& mask, cudaStream_t s) {
-    mask.alloc(R.n_kd4 + 1);
+    mask.alloc_async(R.n_kd4 + 1, s);
     XB_CUDA(cudaMemsetAsync(mask.p, 0, R.n_kd4 + 1, s));
     if (R.n_kd4 > 0) k_kd4_mask<<<grid_for(R.n_kd4, 256), 256, 0, s>>>(R.n_kd4, R.kd4_bin.p, flags, mask.p);
     check_launch("k_kd4_mask");

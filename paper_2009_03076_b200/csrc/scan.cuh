@@ -13,9 +13,30 @@ struct CubTemp {
     }
 };
 
+// CUB scratch from the stream's memory pool (see PoolBuf)
+struct CubPoolTemp {
+    cudaStream_t s;
+    char* p = nullptr;
+    size_t n = 0;
+    explicit CubPoolTemp(cudaStream_t st) : s(st) {}
+    CubPoolTemp(const CubPoolTemp&) = delete;
+    CubPoolTemp& operator=(const CubPoolTemp&) = delete;
+    void* get(size_t bytes) {
+        if (bytes > n) {
+            if (p) XB_CUDA(cudaFreeAsync(p, s));
+            n = bytes ? bytes : 1;
+            XB_CUDA(cudaMallocAsync((void**)&p, n, s));
+        }
+        return p;
+    }
+    ~CubPoolTemp() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
 // out[i] = sum(in[0..i)), n+1 outputs when `in` has n+1 entries with in[n] = 0
-template <class T>
-inline void exclusive_sum(CubTemp& tmp, const T* in, T* out, int64_t n, cudaStream_t s) {
+template <class T, class Tmp>
+inline void exclusive_sum(Tmp& tmp, const T* in, T* out, int64_t n, cudaStream_t s) {
     size_t bytes = 0;
     XB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
     XB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(bytes), bytes, in, out, n, s));
