@@ -53,4 +53,15 @@ for gm in ("central", "clampedCentral", "none"):
     print(f"gradient {gm}: samples {int(st[1])}", flush=True)
 o, d = cam.ray(40, 30)
 print("integrate_ray", integrate_ray(o, d, build_scene(model, regions, tf), tf, params, pixel=30 * 96 + 40)[1])
+# TF edits: active sets rebuilt from the stream-ordered pool and released
+from paper_2009_03076_b200.accel import build_iso_bvh, build_volume_bvh  # noqa: E402
+
+keep = []
+for q in range(6):
+    b = build_volume_bvh(regions, TransferFunction.grayscale((lo, hi), max_alpha=0.2 + 0.1 * q), 0, model=model)
+    c = build_iso_bvh(regions, lo + (q + 1) * (hi - lo) / 8, 0, model=model)
+    if q % 2:
+        keep.append(b)
+    del c
+print("active sets:", [len(b.prims) for b in keep])
 print("sanitize frames done")
