@@ -22,6 +22,26 @@ void build_regions_device(const DevModel& m, DevRegions& out, cudaStream_t s);
 struct xb_cells {
     xb::DevCells c;
 };
+// the builders' private pool per device (common.cuh:PoolScope)
+namespace xb {
+cudaMemPool_t build_pool(int device) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    std::lock_guard<std::mutex> g(mu);
+    XB_CHECK(device >= 0 && device < 64, XB_ERR_ARG, "device index out of range");
+    if (!pools[device]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        XB_CUDA(cudaMemPoolCreate(&pools[device], &props));
+        uint64_t keep = UINT64_MAX;  // trimmed explicitly at each PoolScope's end
+        XB_CUDA(cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &keep));
+    }
+    return pools[device];
+}
+}  // namespace xb
+
 struct xb_model {
     xb::DevModel m;
     // the frame gather's padded copy of each rendered field (march.cuh:kGatherPad), built
@@ -481,6 +501,10 @@ int xb_build_regions(const xb_model* m, xb_regions** out) {
         XB_CHECK(m, XB_ERR_ARG, "null model");
         xb::DeviceGuard g(m->m.device);
         OwnedStream st;
+        // scratch from the builders' pool (common.cuh:PoolScope): C3 regions 0.32-0.99 s
+        // over 8 rebuilds against 0.58-1.5 s through cudaMalloc (build_bricks, whose
+        // 30 GB peak maps faster as a few cudaMalloc blocks, keeps cudaMalloc)
+        xb::PoolScope pool(st.s, m->m.device);
         auto h = std::make_unique<xb_regions>();
         xb::build_regions_device(m->m, h->r, st.s);
         h->model_bricks = m->m.n_bricks;

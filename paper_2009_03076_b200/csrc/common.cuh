@@ -55,24 +55,64 @@ inline void check_launch(const char* what) {
 // ---------------------------------------------------------------------------
 // device buffer (owning, move-only)
 
+// Builder scratch (PoolScope): while a PoolScope is alive on this thread,
+// DevBuf allocations come from a private per-device memory pool on the
+// scope's stream.  The pool keeps what the builder frees (no release
+// threshold), so the level-synchronous builders' grow-and-free cycles reuse
+// mapped memory instead of cudaMalloc / cudaFree (each a device-wide
+// synchronisation and a fresh mapping); the scope's end trims the pool back to
+// what the built object still holds.  Buffers released inside the scope go
+// back with cudaFreeAsync on its stream; buffers that outlive it (the built
+// object) are released later with cudaFree, which accepts pool memory and
+// waits for every stream using it.  Inside the scope every use of its buffers
+// must be on its stream.
+struct PoolCtx {
+    cudaStream_t s = nullptr;
+    cudaMemPool_t pool = nullptr;
+};
+inline PoolCtx& pool_scope() {
+    thread_local PoolCtx c;
+    return c;
+}
+cudaMemPool_t build_pool(int device);  // abi.cu
+struct PoolScope {
+    PoolCtx prev;
+    explicit PoolScope(cudaStream_t s, int device) : prev(pool_scope()) { pool_scope() = PoolCtx{s, build_pool(device)}; }
+    ~PoolScope() {
+        const PoolCtx c = pool_scope();
+        pool_scope() = prev;
+        if (c.pool && cudaStreamSynchronize(c.s) == cudaSuccess) cudaMemPoolTrimTo(c.pool, 0);
+    }
+    PoolScope(const PoolScope&) = delete;
+    PoolScope& operator=(const PoolScope&) = delete;
+};
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t ps = nullptr;  // stream of a pool allocation (PoolScope / alloc_async), else cudaMalloc'd
     DevBuf() = default;
     explicit DevBuf(size_t count) { alloc(count); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), ps(o.ps) { o.p = nullptr; o.n = 0; o.ps = nullptr; }
     DevBuf& operator=(DevBuf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) { release(); p = o.p; n = o.n; ps = o.ps; o.p = nullptr; o.n = 0; o.ps = nullptr; }
         return *this;
     }
     ~DevBuf() { release(); }
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) XB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        if (!count) return;
+        const PoolCtx& c = pool_scope();
+        if (c.pool) {
+            XB_CUDA(cudaMallocFromPoolAsync((void**)&p, count * sizeof(T), c.pool, c.s));
+            ps = c.s;
+        } else {
+            XB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        }
     }
     // from the device's memory pool, ordered on stream s (no implicit device
     // synchronisation, retained pool memory: the TF-edit path); release() is
@@ -81,14 +121,19 @@ struct DevBuf {
         release();
         n = count;
         if (count) XB_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), s));
+        ps = count ? s : nullptr;
     }
     void ensure(size_t count) {  // grow-only
         if (count > n) alloc(count + count / 4 + 64);
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (ps && ps == pool_scope().s) cudaFreeAsync(p, ps);  // scratch, still in its scope
+            else cudaFree(p);
+        }
         p = nullptr;
         n = 0;
+        ps = nullptr;
     }
     void upload(const T* h, size_t count, cudaStream_t s = 0) {  // h: host or device (UVA)
         if (count > n) alloc(count);
