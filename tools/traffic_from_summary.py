@@ -1,7 +1,7 @@
 """profiles/traffic_<cfg>.json from an ncu summary (tools/ncu_summary.py output):
 DRAM bytes (read + write) per launch of the dominant kernel (k_warp) and of the
 other captured frame kernels, for one timed frame.
-python tools/traffic_from_summary.py profiles/r02_v9_ncu_c3.txt c3"""
+python tools/traffic_from_summary.py profiles/r02_v10_ncu_c3.txt c3"""
 import json
 import re
 import sys
