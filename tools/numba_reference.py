@@ -54,7 +54,7 @@ def main():
     tf_ours = bench.tf_for(vr, cfg)
     tf = RTF(tf_ours.domain, tf_ours.rgba)
     t0 = time.perf_counter()
-    scene = r_build_scene(model, regions, tf)
+    scene = r_build_scene(model, regions, tf, iso_value=cfg.get("iso"))
     t_scene = time.perf_counter() - t0
     from paper_2009_03076_b200.model import Box3
 
@@ -82,7 +82,7 @@ def main():
 
         gm, _ = build_bricks(cells)
         gr = build_regions(gm)
-        gs = build_scene(gm, gr, tf_ours)
+        gs = build_scene(gm, gr, tf_ours, iso_value=cfg.get("iso"))
         gf = render_frame(gs, c, tf_ours, MarchParams(seed=0, gradient_mode=cfg["gradient"]))
         out["gpu_vs_reference"] = {
             "rgba8_max_abs_diff": int(np.abs(gf.rgba.astype(int) - fr.rgba.astype(int)).max()),
