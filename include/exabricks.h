@@ -168,6 +168,8 @@ typedef struct {
     int64_t walk2_min;  /* k_walk2 runs when >= walk2_min walks were cut; -1 (default): 500 x SMs */
     int32_t fuse_short; /* 1 (default): short rays run inside k_warp after the long ones; 0: separate k_short */
     int32_t time_march; /* 1: record a CUDA event pair around every k_warp launch (xb_march_times); default 0 */
+    int32_t short_leaves;  /* short ray: complete leaf list of <= short_leaves leaves (default 8) ... */
+    int32_t short_samples; /* ... and <= short_samples estimated samples (default 24) */
 } xb_tuning;
 void xb_tuning_defaults(xb_tuning* t);
 int xb_tuning_get(xb_tuning* t);

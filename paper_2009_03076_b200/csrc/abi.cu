@@ -669,6 +669,8 @@ void xb_tuning_defaults(xb_tuning* t) {
     t->walk2_min = -1;
     t->fuse_short = 1;
     t->time_march = 0;
+    t->short_leaves = xb::kShortLeaves;
+    t->short_samples = (int32_t)xb::kShortSamples;
 }
 
 int xb_tuning_get(xb_tuning* t) {
@@ -687,6 +689,7 @@ int xb_tuning_set(const xb_tuning* t) {
         XB_CHECK(n.leaf_cap >= 0 && n.leaf_cap <= 4096, XB_ERR_ARG, "tuning.leaf_cap out of range");
         XB_CHECK(n.walk_cap1 >= 1, XB_ERR_ARG, "tuning.walk_cap1 must be >= 1");
         XB_CHECK(n.short_rays >= -1 && n.short_rays <= 1, XB_ERR_ARG, "tuning.short_rays must be -1, 0 or 1");
+        XB_CHECK(n.short_leaves >= 1 && n.short_samples >= 1, XB_ERR_ARG, "tuning.short_leaves / short_samples must be >= 1");
         std::lock_guard<std::mutex> g(g_tuning_mu);
         g_tuning = n;
     });
@@ -824,8 +827,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->walk_cap1 = 0;
         A->walk2_min = 0;
         A->cut_list = nullptr;
-        A->short_leaves = xb::kShortLeaves;
-        A->short_samples = xb::kShortSamples;
+        A->short_leaves = T.short_leaves;
+        A->short_samples = (float)T.short_samples;
         A->leaf_cap = 0;
         A->cut_tau = 1;
         if (A->kernel == 0 && T.walk_lists) {
