@@ -216,7 +216,8 @@ void fill_march(xb::MarchConst& M, const xb_march* mp) {
     for (int c = 0; c < 3; c++) M.iso_rgb[c] = mp->iso_rgb[c];
     M.tf_lo = mp->tf_lo;
     M.tf_hi = mp->tf_hi;
-    M.tf_inv = 1.0 / (mp->tf_hi - mp->tf_lo);
+    M.tf_den = mp->tf_hi - mp->tf_lo;
+    M.tf_inv = 1.0 / M.tf_den;
     M.use_tree = mp->use_tree;
     for (int l = 0; l < 32; l++) {
         const double fw = std::ldexp(1.0, l);

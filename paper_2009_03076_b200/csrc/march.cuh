@@ -792,10 +792,23 @@ __device__ __forceinline__ void tf_eval(const double* tf, double tf_lo, double t
     for (int k = 0; k < 4; k++) c[k] = g * tf[i * 4 + k] + f * tf[(i + 1) * 4 + k];
 }
 
-// _tf_eval with the domain reciprocal hoisted: the lerp is continuous across
-// bins, so a last-ulp change of t moves the colour by ~1e-16 only
-__device__ __forceinline__ void tf_eval_fast(const double* tf, double tf_lo, double tf_inv, double v, double c[4]) {
-    double t = (v - tf_lo) * tf_inv;
+// _tf_eval (R/render.py:236-254) with the division by the domain width done
+// through its hoisted reciprocal and 32-byte table loads.  t = (v - lo) / (hi -
+// lo) is still the correctly rounded quotient: q0 = n * (1/d) is within 1 ulp,
+// the residual n - q0 d is exact as one FMA, and q0 + r (1/d) rounded once is
+// RN(n / d) when 1/d is itself correctly rounded (Markstein's theorem; 4e8
+// random pairs incl. boundary significands agree with the division).  Until
+// round 2 the bare q0 was used: a last-ulp change of t moves the colour by
+// ~1e-16 only, but where the reference's alpha is exactly 1 (v at the top of
+// a TF ending opaque) 1 - a ~1e-16 instead of 0 went through the opacity
+// correction 1 - (1 - a)^y with the short first step y < 1 of an eye inside
+// the volume to an alpha of 0.7-0.98 instead of 1 (RGBA off by 0.02, sample
+// counters changed; tests/golden/make_inside.py's frames).  The plain division
+// cost 2 % / 1 % of the C3 / C2 frame, this 2 FMAs.
+__device__ __forceinline__ void tf_eval_fast(const double* tf, double tf_lo, double tf_den, double tf_inv, double v,
+                                             double c[4]) {
+    const double n = v - tf_lo, q0 = n * tf_inv;
+    double t = __fma_rn(__fma_rn(-q0, tf_den, n), tf_inv, q0);
     if (t < 0.0) t = 0.0;
     else if (t > 1.0) t = 1.0;
     const double x = t * 255.0;
@@ -926,12 +939,12 @@ struct MarchConst {
     double iso_value;
     double iso_rgb[3];
     double tf_lo, tf_hi;
+    double tf_den, tf_inv;  // tf_hi - tf_lo, its correctly rounded reciprocal
     // host-computed per finest level (IEEE division on the host, same values
     // as the kernel would compute): dt = fw/(spc*rate), s1 = fw/spc (R/render.py:402-403)
     double lv_dt[32], lv_s1[32], lv_is1[32];
     // 1/dt when dt is a power of two (x / dt == x * (1/dt) exactly), else 0 (divide)
     double lv_idt[32];
-    double tf_inv;  // 1/(tf_hi - tf_lo)
     int use_tree;   // cell-location gather through the split tree (render_frame(use_celllocation=True))
 };
 

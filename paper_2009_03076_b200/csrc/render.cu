@@ -800,7 +800,7 @@ __device__ __forceinline__ void short_ray(const RenderArgs& A, const double* __r
             if (F.den > kEpsWeight) {
                 const double v = F.num / F.den;
                 double c[4];
-                tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_inv, v, c);
+                tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_den, A.M.tf_inv, v, c);
                 if (c[3] > 0.0) {
                     const double alpha = opacity_correct(c[3], sl * A.M.lv_is1[lev]);
                     if (GRAD != 0) {
@@ -1074,7 +1074,7 @@ __global__ void __launch_bounds__(kWarpThreads, MINB) k_warp(const __grid_consta
                             if (F.den > kEpsWeight) {
                                 const double v = F.num / F.den;
                                 double c[4];
-                                tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_inv, v, c);
+                                tf_eval_fast(s_tf, A.M.tf_lo, A.M.tf_den, A.M.tf_inv, v, c);
                                 if (c[3] > 0.0) {
                                     const double alpha = opacity_correct(c[3], sl * A.M.lv_is1[lev]);
                                     if (GRAD != 0) {

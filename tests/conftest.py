@@ -26,7 +26,10 @@ def golden_model(name):
 
 
 def golden_frames():
-    return dict(np.load(GOLDEN / "frames.npz"))
+    """frames.npz (make_golden.py) + frames_inside.npz (make_inside.py: eyes inside the volume)."""
+    fr = dict(np.load(GOLDEN / "frames.npz"))
+    fr.update(np.load(GOLDEN / "frames_inside.npz"))
+    return fr
 
 
 def frame_meta(frames, key):

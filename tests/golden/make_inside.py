@@ -1,0 +1,70 @@
+"""Golden frames with the eye INSIDE the volume (fly-through views), made by
+the reference itself — none of make_golden.py's frames puts the camera inside
+the model, where every ray starts in the middle of an active region (the
+reference's first query starts at t = 0 inside a region box,
+R/accel.py:285-352, and the lattice's first sample is cut at t = 0,
+R/render.py:404-418).  The reference service accepts any camera
+(R/service.py:101-114).
+
+Runs ONLY in the build container (imports the reference read-only):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_inside.py
+
+-> tests/golden/frames_inside.npz, same keys / layout as frames.npz
+(conftest.golden_frames() merges both files, so the oracle's bit-exact frame
+test and the GPU frame-parity matrix pick them up).
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+import make_golden as G  # noqa: E402  (imports the reference)
+
+R = G.R
+
+
+def views(regions):
+    b = regions.bounds
+    lo, hi = np.asarray(b.lo, float), np.asarray(b.hi, float)
+    c = 0.5 * (lo + hi)
+    return [
+        ("inside_centre", c, (1.0, 0.0, 0.0), (0.0, 1.0, 0.0)),
+        ("inside_oblique", c + 0.13 * (hi - lo), (-0.6, -0.5, 0.62), (0.0, 0.0, 1.0)),
+        ("inside_corner", lo + 0.07 * (hi - lo), (1.0, 1.0, 1.0), (0.0, 1.0, 0.0)),
+        ("inside_axis", c, (0.0, 0.0, -1.0), (0.0, 1.0, 0.0)),  # axis-parallel central ray
+    ]
+
+
+def main():
+    out = {}
+    for name, (w, h), max_alpha in (("smoke", (48, 40), 1.0), ("c1", (64, 48), 0.5)):
+        cells = G.avio.generate_synthetic(G.SPECS[name])
+        model, _, regions = G.build_case(name, cells, 32)
+        lo, hi = model.value_range(0)
+        tf = G.TransferFunction.grayscale((lo, hi), max_alpha=max_alpha)
+        scene = R.build_scene(model, regions, tf)
+        for tag, pos, fwd, up in views(regions):
+            cam = R.Camera(pos, fwd, up, 70.0, w, h)
+            key = f"{name}_{tag}"
+            G.store_frame(out, key, scene, cam, tf, R.MarchParams(seed=3, gradient_mode="analytic"))
+            print(key, int(out[f"{key}_px_samples"].sum()), "samples")
+        if name == "smoke":  # iso surface + volume (make_golden's smoke_iso) seen from inside
+            iso_v = float(lo + 0.45 * (hi - lo))
+            g05 = G.TransferFunction.grayscale((lo, hi), max_alpha=0.5)
+            si = R.build_scene(model, regions, g05, iso_value=iso_v)
+            for tag, pos, fwd, up in views(regions)[:3]:
+                key = f"{name}_{tag}_iso"
+                G.store_frame(out, key, si, R.Camera(pos, fwd, up, 70.0, w, h), g05,
+                              R.MarchParams(seed=1, early_term_threshold=0.9), iso=iso_v)
+                print(key, int(out[f"{key}_px_samples"].sum()), "samples")
+    np.savez_compressed(G.OUT / "frames_inside.npz", **out)
+
+
+if __name__ == "__main__":
+    sys.setrecursionlimit(100000)
+    main()

@@ -296,3 +296,4 @@ def test_reference_renderer_pixel_identical_c1():
         assert (ours.stats.regions, ours.stats.samples) == (theirs.stats.regions, theirs.stats.samples)
         assert np.abs(ours.rgba.astype(int) - theirs.rgba.astype(int)).max() <= 1
         assert np.count_nonzero(ours.rgba != theirs.rgba) <= ours.rgba.size // 10000
+
