@@ -62,6 +62,37 @@ def main():
                 G.store_frame(out, key, si, R.Camera(pos, fwd, up, 70.0, w, h), g05,
                               R.MarchParams(seed=1, early_term_threshold=0.9), iso=iso_v)
                 print(key, int(out[f"{key}_px_samples"].sum()), "samples")
+    # ---- edge cases of the march arguments (also none in make_golden.py)
+    cells = G.avio.generate_synthetic(G.SPECS["c1"])
+    model, _, regions = G.build_case("c1", cells, 32)
+    lo, hi = model.value_range(0)
+    b = regions.bounds
+    blo, bhi = np.asarray(b.lo, float), np.asarray(b.hi, float)
+    c = np.floor(0.5 * (blo + bhi))  # integer coordinates: on cell / region faces
+    g = G.TransferFunction.grayscale((lo, hi), max_alpha=0.7)
+    scene = R.build_scene(model, regions, g)
+    edge = [
+        # odd size: the centre ray is exactly (0, 0, 1) through region faces (zero-direction slab rule)
+        ("edge_axis_out", R.Camera([c[0], c[1], blo[2] - 9.0], [0.0, 0.0, 1.0], [0.0, 1.0, 0.0], 30.0, 33, 31),
+         R.MarchParams(seed=5, gradient_mode="analytic")),
+        ("edge_axis_in", R.Camera(c, [0.0, 1.0, 0.0], [1.0, 0.0, 0.0], 50.0, 31, 33),
+         R.MarchParams(seed=5, gradient_mode="central")),
+        # coarse steps, no early termination, the largest seed, non-square frame
+        ("edge_coarse", R.Camera(c + [0.3, -0.2, 0.1], [0.3, 0.2, 1.0], [0.0, 1.0, 0.0], 60.0, 40, 17),
+         R.MarchParams(samples_per_cell=1.0, rate_scale=0.3, early_term_threshold=1.0, seed=2**64 - 1,
+                       gradient_mode="analytic")),
+        # fine steps, eye inside behind two clip planes, clamped central gradients
+        ("edge_clip_in", R.Camera(c + [1.5, 0.5, -0.5], [-1.0, 0.1, 0.4], [0.0, 1.0, 0.0], 80.0, 24, 24),
+         R.MarchParams(samples_per_cell=3.0, rate_scale=1.9, seed=77, gradient_mode="clampedCentral",
+                       clip_planes=[((1.0, 0.0, 0.0), float(c[0]) - 3.0), ((0.2, -1.0, 0.3), -float(c[1]) - 4.0)])),
+        # a one-pixel-wide frame
+        ("edge_column", R.Camera(c + [0.5, 0.5, 0.5], [0.0, 0.0, -1.0], [0.0, 1.0, 0.0], 90.0, 1, 9),
+         R.MarchParams(seed=11, gradient_mode="none")),
+    ]
+    for tag, cam, params in edge:
+        key = f"c1_{tag}"
+        G.store_frame(out, key, scene, cam, g, params)
+        print(key, int(out[f"{key}_px_samples"].sum()), "samples")
     np.savez_compressed(G.OUT / "frames_inside.npz", **out)
 
 
