@@ -170,6 +170,8 @@ typedef struct {
     int32_t time_march; /* 1: record a CUDA event pair around every k_warp launch (xb_march_times); default 0 */
     int32_t short_leaves;  /* short ray: complete leaf list of <= short_leaves leaves (default 8) ... */
     int32_t short_samples; /* ... and <= short_samples estimated samples (default 24) */
+    int32_t grab_div;      /* k_warp's guided ray grabs: remaining / (grab_div x warps), in [1, 32] (default 4) */
+    int32_t grab_fixed;    /* > 0: fixed grabs of that many rays instead (default 0) */
 } xb_tuning;
 void xb_tuning_defaults(xb_tuning* t);
 int xb_tuning_get(xb_tuning* t);

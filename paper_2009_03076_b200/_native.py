@@ -58,7 +58,7 @@ class XbTuning(C.Structure):
 
     _fields_ = [("kernel", i32), ("traversal", i32), ("walk_lists", i32), ("leaf_cap", i32), ("walk_cap1", i32),
                 ("short_rays", i32), ("walk2_min", i64), ("fuse_short", i32), ("time_march", i32),
-                ("short_leaves", i32), ("short_samples", i32)]
+                ("short_leaves", i32), ("short_samples", i32), ("grab_div", i32), ("grab_fixed", i32)]
 
 
 # exported symbol -> (restype, argtypes); tests check every declared symbol

@@ -672,6 +672,8 @@ void xb_tuning_defaults(xb_tuning* t) {
     t->time_march = 0;
     t->short_leaves = xb::kShortLeaves;
     t->short_samples = (int32_t)xb::kShortSamples;
+    t->grab_div = 4;
+    t->grab_fixed = 0;
 }
 
 int xb_tuning_get(xb_tuning* t) {
@@ -691,6 +693,8 @@ int xb_tuning_set(const xb_tuning* t) {
         XB_CHECK(n.walk_cap1 >= 1, XB_ERR_ARG, "tuning.walk_cap1 must be >= 1");
         XB_CHECK(n.short_rays >= -1 && n.short_rays <= 1, XB_ERR_ARG, "tuning.short_rays must be -1, 0 or 1");
         XB_CHECK(n.short_leaves >= 1 && n.short_samples >= 1, XB_ERR_ARG, "tuning.short_leaves / short_samples must be >= 1");
+        XB_CHECK(n.grab_div >= 1 && n.grab_fixed >= 0 && n.grab_fixed <= 32, XB_ERR_ARG,
+                 "tuning.grab_div must be >= 1 and grab_fixed in [0, 32]");
         std::lock_guard<std::mutex> g(g_tuning_mu);
         g_tuning = n;
     });
@@ -807,8 +811,8 @@ int xb_render(const xb_model* m, const xb_regions* r, int32_t field, const xb_ac
         A->dbg = xb::kDebugChunks ? scratch + 9 : nullptr;  // [9, 16): make DEBUG_CHUNKS=1 builds only
         A->short_counter = scratch + 16;
         A->fuse_short = T.fuse_short != 0;
-        A->grab_div = 4;
-        A->grab_fixed = 0;
+        A->grab_div = T.grab_div;
+        A->grab_fixed = T.grab_fixed;
         double* iso_buf = nullptr;
         if (A->M.iso_on) {
             const size_t n_slots = (size_t)n_local * xb::kTileW * xb::kTileH;

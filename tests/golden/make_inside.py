@@ -93,6 +93,26 @@ def main():
         key = f"c1_{tag}"
         G.store_frame(out, key, scene, cam, g, params)
         print(key, int(out[f"{key}_px_samples"].sum()), "samples")
+    # ---- edge cases of the transfer function / iso value, from an orbit view
+    cam = G.orbit_cameras(regions.bounds, 8, 40, 36)[3]
+    zero = np.tile(np.linspace(0.0, 1.0, 256)[:, None], (1, 4))
+    zero[:, 3] = 0.0  # nothing active: every ray misses
+    top = np.tile(np.linspace(0.0, 1.0, 256)[:, None], (1, 4))
+    top[:, 3] = 0.2
+    top[255, 3] = 1.0  # opaque only at the top: alpha exactly 1 behind short last steps
+    tfs = [
+        ("tf_empty", G.TransferFunction((lo, hi), zero), None, "analytic"),
+        ("tf_top_opaque", G.TransferFunction((lo, hi), top), None, "analytic"),
+        # domain below most values: samples clamp to the last (opaque) entry
+        ("tf_narrow", G.TransferFunction.grayscale((lo, lo + 0.3 * (hi - lo)), max_alpha=1.0), None, "central"),
+        ("iso_above_range", g, float(hi + 1.0), "analytic"),  # no iso candidates at all
+        ("iso_at_max", g, float(hi), "none"),
+    ]
+    for tag, tf, iso, mode in tfs:
+        sc = R.build_scene(model, regions, tf, iso_value=iso)
+        key = f"c1_edge_{tag}"
+        G.store_frame(out, key, sc, cam, tf, R.MarchParams(seed=9, gradient_mode=mode), iso=iso)
+        print(key, int(out[f"{key}_px_samples"].sum()), "samples")
     np.savez_compressed(G.OUT / "frames_inside.npz", **out)
 
 

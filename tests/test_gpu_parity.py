@@ -289,6 +289,7 @@ KERNEL_VARIANTS = {  # xb_tuning fields (include/exabricks.h) of each frame-pipe
     "warp_short": {"short_rays": 1},             # short rays one per lane (k_warp's second phase) even when few
     "warp_kshort": {"short_rays": 1, "fuse_short": 0},  # ... through the separate k_short launch
     "warp_2pass": {"walk_cap1": 2, "walk2_min": 0},     # k_walk2 continues (nearly) every walk
+    "warp_grab8": {"grab_fixed": 8},             # fixed 8-ray grabs instead of the guided schedule
     "warp_wide_short": {"short_rays": 1, "short_leaves": 16, "short_samples": 4096},  # every complete list lane-per-ray
     "tile": {"kernel": 1},                       # one thread per pixel
     "lbvh": {"traversal": 1},                    # per-visit LBVH closest-hit queries (the reference's traversal)
