@@ -20,12 +20,13 @@ from paper_2009_03076_b200.bricks import BrickBuildParams, build_bricks  # noqa:
 from paper_2009_03076_b200.model import CellList  # noqa: E402
 from paper_2009_03076_b200.orbit import orbit_cameras  # noqa: E402
 from paper_2009_03076_b200.regions import build_regions  # noqa: E402
-from paper_2009_03076_b200.render import MarchParams, build_scene, integrate_ray, render_frame_float  # noqa: E402
+from paper_2009_03076_b200.render import Camera, MarchParams, build_scene, integrate_ray, render_frame_float  # noqa: E402
 from tests_util import golden_cells  # noqa: E402
 
 VARIANTS = {"warp": {}, "warp_cap1": {"leaf_cap": 1}, "warp_nowalk": {"walk_lists": 0}, "warp_short": {"short_rays": 1},
             "warp_kshort": {"short_rays": 1, "fuse_short": 0}, "warp_2pass": {"walk_cap1": 2, "walk2_min": 0},
-            "tile": {"kernel": 1}, "lbvh": {"traversal": 1}}
+            "warp_wide_short": {"short_rays": 1, "short_leaves": 16, "short_samples": 4096},
+            "warp_grab8": {"grab_fixed": 8}, "tile": {"kernel": 1}, "lbvh": {"traversal": 1}}
 
 i, j, k, lev, vals = golden_cells("smoke")
 model, tree = build_bricks(CellList(i, j, k, lev, vals), BrickBuildParams(keep_split_tree=True))
@@ -34,7 +35,9 @@ lo, hi = model.value_range(0)
 tf = TransferFunction.grayscale((lo, hi), max_alpha=0.5)
 cam = orbit_cameras(regions.bounds, 4, 96, 64)[1]
 params = MarchParams(seed=3, gradient_mode="analytic")
-for iso in (None, 0.5 * (lo + hi)):
+b = regions.bounds
+inside = Camera(0.5 * (np.asarray(b.lo) + np.asarray(b.hi)), (-0.6, -0.5, 0.62), (0.0, 0.0, 1.0), 70.0, 48, 40)
+for iso, cam in ((None, cam), (0.5 * (lo + hi), cam), (None, inside), (0.45 * (lo + hi), inside)):
     scene = build_scene(model, regions, tf, iso_value=iso, tree=tree)
     ref = None
     for name, fields in VARIANTS.items():
