@@ -133,7 +133,10 @@ __global__ void __launch_bounds__(128) k_iso_pass(const __grid_constant__ Render
 // 448-449).  The scan reassociates the alpha recurrence, so alpha differs from
 // the reference by rounding only (~1e-16), like CUDA's pow.
 
-constexpr int kWarpThreads = 128;
+#ifndef XB_WARP_THREADS
+#define XB_WARP_THREADS 128
+#endif
+constexpr int kWarpThreads = XB_WARP_THREADS;
 #ifndef XB_WARP_MINB
 #define XB_WARP_MINB 4
 #endif
