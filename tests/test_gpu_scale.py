@@ -336,3 +336,34 @@ def test_integrate_ray_from_inside_matches_oracle():
         assert gs == ws, q
         samples += ws["samples"]
     assert samples > 0
+
+
+def test_iso_intersect_from_inside_matches_oracle():
+    """iso_intersect (R/render.py:635-651) for rays starting inside the volume:
+    hit / miss, t_hit and the gradient at the hit equal the oracle's."""
+    from paper_2009_03076_b200.accel import TransferFunction, build_iso_bvh
+    from paper_2009_03076_b200.render import MarchParams, build_scene, iso_intersect
+
+    bench = _bench()
+    cfg = bench.CONFIGS["c1"]
+    model, regions = _build(bench.make_cells(cfg))
+    lo, hi = model.value_range(0)
+    iso = float(lo + 0.4 * (hi - lo))
+    scene = build_scene(model, regions, TransferFunction.grayscale((lo, hi)), iso_value=iso)
+    bvh = build_iso_bvh(regions, iso, 0, model=model)
+    osc = _oracle_scene(model, regions)
+    b = regions.bounds
+    blo, bhi = np.asarray(b.lo, float), np.asarray(b.hi, float)
+    rng = np.random.default_rng(23)
+    hits = 0
+    for q in range(80):
+        o = blo + rng.random(3) * (bhi - blo)
+        d = rng.normal(size=3) if q % 8 else np.eye(3)[q % 3]
+        got = iso_intersect(o, d, bvh, scene, iso, params=MarchParams(seed=6), pixel=q)
+        want = osc.iso_intersect(o, d, iso, seed=6, pixel=q)
+        assert (got is None) == (want is None), q
+        if want is not None:
+            hits += 1
+            assert got[0] == want[0], q
+            assert np.array_equal(got[1], want[1]), q
+    assert hits > 0
